@@ -1,0 +1,32 @@
+"""B200-native SPC5 beta(r, vs) sparse matrix/vector product (arXiv 2307.14774).
+
+Drop-in for the hot path of the reference package ``spc5``
+(/root/reference/pkg/src/spc5/__init__.py:11-21 names): CSR->SPC5 conversion,
+the SpMV entry points, the nnz-balanced partition and the timing harness,
+backed by hand-written sm_100a CUDA kernels in ``libspc5_b200.so`` (C ABI:
+include/spc5_b200.h).  Importing this package loads the library; there is no
+CPU fallback.
+"""
+
+from . import _native  # noqa: F401  (loads libspc5_b200.so, raises ImportError if absent)
+from .blocks import (VALID_R, VALID_VS, FillingStats, Spc5Matrix, csr_to_spc5,
+                     csr_to_spc5_device, filling_stats, footprint_comparison, load_spc5,
+                     mask_dtype, save_spc5, spc5_to_csr, validate_spc5)
+from .harness import BenchRecord, ValidationError, run_bench, run_kernel
+from .kernels import (KernelConfig, SpmvResult, VerifyReport, block_value_offsets,
+                      csr_reference, mask_popcounts, spmv, spmv_spc5_scalar, spmv_spc5_vector,
+                      verify_against_oracle)
+from .mmio import CsrMatrix, make_dense, make_identity, make_random
+from .parallel import Partition, partition_by_nnz, spmv_parallel
+
+__version__ = "0.1.0"
+
+__all__ = [
+    "BenchRecord", "CsrMatrix", "FillingStats", "KernelConfig", "Partition", "Spc5Matrix",
+    "SpmvResult", "VALID_R", "VALID_VS", "ValidationError", "VerifyReport",
+    "block_value_offsets", "csr_reference", "csr_to_spc5", "csr_to_spc5_device",
+    "filling_stats", "footprint_comparison", "load_spc5", "make_dense", "make_identity",
+    "make_random", "mask_dtype", "mask_popcounts", "partition_by_nnz", "run_bench",
+    "run_kernel", "save_spc5", "spc5_to_csr", "spmv", "spmv_parallel", "spmv_spc5_scalar",
+    "spmv_spc5_vector", "validate_spc5", "verify_against_oracle",
+]

@@ -1,0 +1,358 @@
+// capi.cu -- the extern "C" boundary (include/spc5_b200.h).
+//
+// Handles own their device arrays; every entry point validates its arguments
+// the way the reference Python functions do (blocks.py:89-93,
+// kernels.py:99-103, 219-223) and reports through an int status plus a
+// thread-local message (spc5_last_error).
+#include <cuda_runtime.h>
+
+#include <mutex>
+#include <new>
+#include <string>
+
+#include "common.cuh"
+
+struct spc5_matrix {
+    spc5::Matrix m;
+    std::mutex plan_mu;
+};
+
+namespace spc5 {
+
+static thread_local std::string g_err;
+static thread_local int g_launches = 0;
+
+void set_error(const std::string &msg) { g_err = msg; }
+int fail(int status, const std::string &msg) {
+    g_err = msg;
+    return status;
+}
+int cuda_fail(cudaError_t e, const char *what) {
+    g_err = std::string("CUDA error ") + cudaGetErrorName(e) + " (" + cudaGetErrorString(e) +
+            ") in " + what;
+    return e == cudaErrorMemoryAllocation ? SPC5_ENOMEM : SPC5_ECUDA;
+}
+void note_launches(int n) { g_launches += n; }
+
+int dev_alloc(void **p, size_t bytes) {
+    *p = nullptr;
+    if (bytes == 0) bytes = 64;
+    cudaError_t e = cudaMalloc(p, bytes);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *p = nullptr;
+        return cuda_fail(e, "cudaMalloc");
+    }
+    return SPC5_OK;
+}
+void dev_free(void *p) {
+    if (p) cudaFree(p);
+}
+
+static int check_shape(int r, int vs, int precision) {
+    if (r != 1 && r != 2 && r != 4 && r != 8)
+        return fail(SPC5_EINVAL, "r must be one of (1, 2, 4, 8), got " + std::to_string(r));
+    if (vs != 4 && vs != 8 && vs != 16)
+        return fail(SPC5_EINVAL, "vs must be one of (4, 8, 16), got " + std::to_string(vs));
+    if (precision != SPC5_F32 && precision != SPC5_F64)
+        return fail(SPC5_EINVAL, "precision must be 'f32' or 'f64'");
+    return SPC5_OK;
+}
+
+static void free_matrix(Matrix &m) {
+    free_plan(m.plan);
+    dev_free(m.rowptr);
+    dev_free(m.colidx);
+    dev_free(m.masks);
+    dev_free(m.values);
+    dev_free(m.dx);
+    dev_free(m.dy);
+    m.rowptr = nullptr;
+    m.colidx = nullptr;
+    m.masks = m.values = m.dx = m.dy = nullptr;
+}
+
+static void init_common(Matrix &m, int64_t num_rows, int64_t num_cols, int r, int vs,
+                        int precision, int64_t block_base) {
+    m.num_rows = num_rows;
+    m.num_cols = num_cols;
+    m.r = r;
+    m.vs = vs;
+    m.precision = precision;
+    m.num_panels = (num_rows + r - 1) / r;
+    m.block_base = block_base;
+    cudaGetDevice(&m.device);
+    int sms = 0;
+    if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, m.device) == cudaSuccess &&
+        sms > 0)
+        m.sm_count = sms;
+    cudaGetLastError();
+}
+
+static int ensure_plan(spc5_matrix *h, cudaStream_t st) {
+    if (h->m.plan.built) return SPC5_OK;
+    std::lock_guard<std::mutex> lk(h->plan_mu);
+    if (h->m.plan.built) return SPC5_OK;
+    int s = build_plan(h->m, /*validate=*/true, st);
+    if (s != SPC5_OK) {
+        std::string keep = g_err;
+        free_plan(h->m.plan);
+        g_err = keep;
+    }
+    return s;
+}
+
+}  // namespace spc5
+
+using namespace spc5;
+
+extern "C" {
+
+int spc5_version(void) { return 10000; }
+
+const char *spc5_last_error(void) { return g_err.c_str(); }
+
+int spc5_last_launch_count(void) { return g_launches; }
+
+int spc5_device_count(int *count) {
+    *count = 0;
+    cudaError_t e = cudaGetDeviceCount(count);
+    if (e != cudaSuccess) {
+        cudaGetLastError();
+        *count = 0;
+        return cuda_fail(e, "cudaGetDeviceCount");
+    }
+    return SPC5_OK;
+}
+
+int spc5_convert_csr(int64_t num_rows, int64_t num_cols, int64_t nnz, int precision, int r,
+                     int vs, const int64_t *d_row_ptr, const int32_t *d_col_idx,
+                     const void *d_values, int64_t block_base, void *stream,
+                     spc5_matrix_t *out) {
+    g_launches = 0;
+    *out = nullptr;
+    SPC5_TRY(check_shape(r, vs, precision));
+    if (num_rows < 0 || num_cols < 0 || nnz < 0)
+        return fail(SPC5_EINVAL, "dimensions must be non-negative");
+    if (num_cols > (int64_t)INT32_MAX + 1)
+        return fail(SPC5_EINVAL, "num_cols exceeds the int32 column index range");
+    auto *h = new (std::nothrow) spc5_matrix();
+    if (!h) return fail(SPC5_ENOMEM, "out of host memory");
+    Matrix &m = h->m;
+    init_common(m, num_rows, num_cols, r, vs, precision, block_base);
+    m.nnz = nnz;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    int s = convert_csr(m, d_row_ptr, d_col_idx, d_values, st);
+    if (s == SPC5_OK) s = build_plan(m, /*validate=*/false, st);
+    if (s != SPC5_OK) {
+        std::string keep = g_err;
+        free_matrix(m);
+        delete h;
+        g_err = keep;
+        return s;
+    }
+    *out = h;
+    return SPC5_OK;
+}
+
+int spc5_import(int64_t num_rows, int64_t num_cols, int r, int vs, int precision,
+                int64_t num_blocks, int64_t nnz, const int64_t *rowptr, const uint32_t *colidx,
+                const void *masks, const void *values, int from_host, int64_t block_base,
+                void *stream, spc5_matrix_t *out) {
+    g_launches = 0;
+    *out = nullptr;
+    SPC5_TRY(check_shape(r, vs, precision));
+    if (num_rows < 0 || num_cols < 0 || nnz < 0 || num_blocks < 0)
+        return fail(SPC5_EINVAL, "dimensions must be non-negative");
+    auto *h = new (std::nothrow) spc5_matrix();
+    if (!h) return fail(SPC5_ENOMEM, "out of host memory");
+    Matrix &m = h->m;
+    init_common(m, num_rows, num_cols, r, vs, precision, block_base);
+    m.num_blocks = num_blocks;
+    m.nnz = nnz;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const cudaMemcpyKind kind = from_host ? cudaMemcpyHostToDevice : cudaMemcpyDeviceToDevice;
+    auto body = [&]() -> int {
+        SPC5_TRY(dev_alloc(&m.rowptr, (size_t)m.num_panels + 1));
+        SPC5_TRY(dev_alloc(&m.colidx, (size_t)num_blocks));
+        SPC5_TRY(dev_alloc(reinterpret_cast<uint8_t **>(&m.masks),
+                           (size_t)(num_blocks * r * m.mask_bytes())));
+        SPC5_TRY(dev_alloc(reinterpret_cast<uint8_t **>(&m.values),
+                           (size_t)(nnz * m.value_bytes())));
+        SPC5_CUDA(cudaMemcpyAsync(m.rowptr, rowptr, sizeof(int64_t) * (m.num_panels + 1), kind, st));
+        if (num_blocks) {
+            SPC5_CUDA(cudaMemcpyAsync(m.colidx, colidx, sizeof(uint32_t) * num_blocks, kind, st));
+            SPC5_CUDA(cudaMemcpyAsync(m.masks, masks, (size_t)num_blocks * r * m.mask_bytes(),
+                                      kind, st));
+        }
+        if (nnz)
+            SPC5_CUDA(cudaMemcpyAsync(m.values, values, (size_t)nnz * m.value_bytes(), kind, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        return SPC5_OK;
+    };
+    int s = body();
+    if (s != SPC5_OK) {
+        std::string keep = g_err;
+        free_matrix(m);
+        delete h;
+        g_err = keep;
+        return s;
+    }
+    *out = h;
+    return SPC5_OK;
+}
+
+int spc5_info(spc5_matrix_t h, spc5_info_t *info) {
+    if (!h || !info) return fail(SPC5_EINVAL, "null handle");
+    const Matrix &m = h->m;
+    info->num_rows = m.num_rows;
+    info->num_cols = m.num_cols;
+    info->num_panels = m.num_panels;
+    info->num_blocks = m.num_blocks;
+    info->nnz = m.nnz;
+    info->r = m.r;
+    info->vs = m.vs;
+    info->precision = m.precision;
+    info->mask_bytes = m.mask_bytes();
+    info->block_base = m.block_base;
+    info->num_chunks = m.plan.num_chunks;
+    info->num_split_chunks = m.plan.num_split;
+    // blocks.py:180-183 (4-byte declared index width)
+    info->footprint_bytes = m.nnz * m.value_bytes() + m.num_blocks * 4 +
+                            m.num_blocks * m.r * m.mask_bytes() + (m.num_panels + 1) * 4;
+    return SPC5_OK;
+}
+
+int spc5_prepare(spc5_matrix_t h, void *stream) {
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    g_launches = 0;
+    return ensure_plan(h, static_cast<cudaStream_t>(stream));
+}
+
+int spc5_export(spc5_matrix_t h, int64_t *rowptr, uint32_t *colidx, void *masks, void *values,
+                int to_host, void *stream) {
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    const Matrix &m = h->m;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    const cudaMemcpyKind kind = to_host ? cudaMemcpyDeviceToHost : cudaMemcpyDeviceToDevice;
+    if (rowptr)
+        SPC5_CUDA(cudaMemcpyAsync(rowptr, m.rowptr, sizeof(int64_t) * (m.num_panels + 1), kind, st));
+    if (colidx && m.num_blocks)
+        SPC5_CUDA(cudaMemcpyAsync(colidx, m.colidx, sizeof(uint32_t) * m.num_blocks, kind, st));
+    if (masks && m.num_blocks)
+        SPC5_CUDA(cudaMemcpyAsync(masks, m.masks, (size_t)m.num_blocks * m.r * m.mask_bytes(),
+                                  kind, st));
+    if (values && m.nnz)
+        SPC5_CUDA(cudaMemcpyAsync(values, m.values, (size_t)m.nnz * m.value_bytes(), kind, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    return SPC5_OK;
+}
+
+int spc5_device_arrays(spc5_matrix_t h, const int64_t **rowptr, const uint32_t **colidx,
+                       const void **masks, const void **values) {
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    if (rowptr) *rowptr = h->m.rowptr;
+    if (colidx) *colidx = h->m.colidx;
+    if (masks) *masks = h->m.masks;
+    if (values) *values = h->m.values;
+    return SPC5_OK;
+}
+
+int spc5_spmv(spc5_matrix_t h, const void *d_x, void *d_y, int accumulate, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    if ((!d_x && h->m.num_cols) || (!d_y && h->m.num_rows))
+        return fail(SPC5_EINVAL, "x/y must be non-null");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SPC5_TRY(ensure_plan(h, st));
+    return launch_spmv(h->m, 0, h->m.num_panels, d_x, d_y, accumulate, st);
+}
+
+int spc5_spmv_panels(spc5_matrix_t h, int64_t panel_lo, int64_t panel_hi, const void *d_x,
+                     void *d_y, int accumulate, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    if (panel_lo < 0 || panel_hi < panel_lo || panel_hi > h->m.num_panels)
+        return fail(SPC5_EINVAL, "panel range out of bounds");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SPC5_TRY(ensure_plan(h, st));
+    if (panel_lo == panel_hi) return SPC5_OK;
+    return launch_spmv(h->m, panel_lo, panel_hi, d_x, d_y, accumulate, st);
+}
+
+int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    Matrix &m = h->m;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SPC5_TRY(ensure_plan(h, st));
+    const size_t xb = (size_t)m.num_cols * m.value_bytes(), yb = (size_t)m.num_rows * m.value_bytes();
+    {
+        std::lock_guard<std::mutex> lk(h->plan_mu);
+        if (!m.dx) SPC5_TRY(dev_alloc(&m.dx, xb));
+        if (!m.dy) SPC5_TRY(dev_alloc(&m.dy, yb));
+    }
+    if (xb) SPC5_CUDA(cudaMemcpyAsync(m.dx, h_x, xb, cudaMemcpyHostToDevice, st));
+    if (accumulate && yb) SPC5_CUDA(cudaMemcpyAsync(m.dy, h_y, yb, cudaMemcpyHostToDevice, st));
+    SPC5_TRY(launch_spmv(m, 0, m.num_panels, m.dx, m.dy, accumulate, st));
+    if (yb) SPC5_CUDA(cudaMemcpyAsync(h_y, m.dy, yb, cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    return SPC5_OK;
+}
+
+int spc5_partition_by_nnz(spc5_matrix_t h, int workers, int64_t *h_ranges, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    if (workers < 1) return fail(SPC5_EINVAL, "workers must be >= 1");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SPC5_TRY(ensure_plan(h, st));
+    return partition_by_nnz(h->m, workers, h_ranges, st);
+}
+
+int spc5_block_value_offsets(spc5_matrix_t h, int64_t *d_offsets, void *stream) {
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    return block_value_offsets(h->m, d_offsets, static_cast<cudaStream_t>(stream));
+}
+
+int spc5_validate(spc5_matrix_t h, void *stream) {
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    return validate_structure(h->m, static_cast<cudaStream_t>(stream));
+}
+
+int spc5_to_csr(spc5_matrix_t h, int64_t *d_row_ptr, int32_t *d_col_idx, void *d_values,
+                void *stream) {
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    return to_csr(h->m, d_row_ptr, d_col_idx, d_values, static_cast<cudaStream_t>(stream));
+}
+
+int spc5_free(spc5_matrix_t h) {
+    if (!h) return SPC5_OK;
+    free_matrix(h->m);
+    delete h;
+    return SPC5_OK;
+}
+
+int spc5_csr_exact(int64_t num_rows, int precision, const int64_t *d_row_ptr,
+                   const int32_t *d_col_idx, const void *d_values, const void *d_x, double *d_y,
+                   double *d_abs, void *stream) {
+    if (precision != SPC5_F32 && precision != SPC5_F64)
+        return fail(SPC5_EINVAL, "precision must be 'f32' or 'f64'");
+    return csr_exact(num_rows, precision, d_row_ptr, d_col_idx, d_values, d_x, d_y, d_abs,
+                     static_cast<cudaStream_t>(stream));
+}
+
+int spc5_gen_stencil27_rowptr(int64_t n, int64_t row_lo, int64_t row_hi, int64_t *d_row_ptr,
+                              void *stream) {
+    return gen_stencil27_rowptr(n, row_lo, row_hi, d_row_ptr, static_cast<cudaStream_t>(stream));
+}
+
+int spc5_gen_stencil27_fill(int64_t n, int64_t row_lo, int64_t row_hi, int precision,
+                            uint64_t seed, double diag, const int64_t *d_row_ptr,
+                            int32_t *d_col_idx, void *d_values, void *stream) {
+    if (precision != SPC5_F32 && precision != SPC5_F64)
+        return fail(SPC5_EINVAL, "precision must be 'f32' or 'f64'");
+    return gen_stencil27_fill(n, row_lo, row_hi, precision, seed, diag, d_row_ptr, d_col_idx,
+                              d_values, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

@@ -1,0 +1,465 @@
+// plan.cu -- K3: popcount prefix, structural checks, the SpMV work plan and
+// partition_by_nnz, all on the device.
+//
+//  * mask_popcounts / block_value_offsets (kernels.py:82-96): per-tile
+//    popcount sums (kTile blocks) + an exclusive scan; the value offset of any
+//    block b is tile_prefix[b / kTile] + a warp popcount over < kTile blocks.
+//  * The SpMV plan cuts the block array into chunks (one warp each).  Chunk
+//    starts are panel starts (targets every CB blocks snapped back to the
+//    start of the panel holding them) plus, inside panels longer than kSplit
+//    blocks, the GLOBAL multiples of kSplit.  A panel is therefore split only
+//    where its own length and global position say so, never where the chunk
+//    size does, which keeps y bitwise independent of the plan granularity,
+//    of spmv_parallel ranges and of row-panel sharding across GPUs.
+//  * partition_by_nnz (parallel.py:31-52): boundary_k =
+//    searchsorted(cum, total*k/P, 'left') + 1 with cum[p] = nnz up to the end
+//    of panel p, clamped to num_panels; one warp binary-searches each target.
+//  * validate_spc5 (blocks.py:201-232): same checks, same messages, same order.
+#include <cub/cub.cuh>
+#include <thrust/iterator/counting_iterator.h>
+#include <thrust/iterator/transform_iterator.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "common.cuh"
+
+namespace spc5 {
+int scan_inclusive_i64(const int64_t *in, int64_t *out, int64_t n, cudaStream_t st);
+
+namespace {
+
+__global__ void tile_sums_kernel(int64_t nb, int r, int vs, const void *__restrict__ masks,
+                                 int64_t num_tiles, int64_t *tile_sums) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t t = warp; t < num_tiles; t += nwarps) {
+        const int64_t lo = t * kTile * r, hi = std::min<int64_t>((t + 1) * kTile, nb) * r;
+        int s = 0;
+        for (int64_t i = lo + lane; i < hi; i += 32) s += __popc(load_mask(masks, i, vs));
+        s = __reduce_add_sync(0xffffffffu, s);
+        if (lane == 0) tile_sums[t] = s;
+    }
+}
+
+// value offset of block b, computed by a full warp
+__device__ int64_t warp_value_offset(int64_t b, int r, int vs, const void *masks,
+                                     const int64_t *tile_prefix) {
+    const int lane = threadIdx.x & 31;
+    const int64_t t = b / kTile;
+    int s = 0;
+    for (int64_t i = t * kTile * r + lane; i < b * r; i += 32) s += __popc(load_mask(masks, i, vs));
+    s = __reduce_add_sync(0xffffffffu, s);
+    return tile_prefix[t] + s;
+}
+
+// first index i in [0, n] with a[i] > key (a non-decreasing)
+__device__ __forceinline__ int64_t upper_bound_dev(const int64_t *a, int64_t n, int64_t key) {
+    int64_t lo = 0, hi = n + 1;
+    while (lo < hi) {
+        const int64_t mid = lo + (hi - lo) / 2;
+        if (a[mid] <= key) lo = mid + 1;
+        else hi = mid;
+    }
+    return lo;
+}
+
+// structural checks over panels (thread per panel)
+struct CheckOut {
+    unsigned long long popc;
+    int rowptr_bad;      // non-decreasing / start
+    int bits_beyond;     // mask >> vs != 0
+    int anchor_missing;  // OR of the block's masks lacks bit 0
+    int past_end;        // set bit maps to column >= num_cols
+    long long first_unsorted_panel;
+};
+
+__global__ void check_kernel(int64_t num_panels, int64_t nb, int64_t num_cols, int r, int vs,
+                             const int64_t *__restrict__ rowptr,
+                             const uint32_t *__restrict__ colidx,
+                             const void *__restrict__ masks, CheckOut *out) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= num_panels) return;
+    const int64_t s = rowptr[p], e = rowptr[p + 1];
+    if (e < s || s < 0 || e > nb || (p == 0 && s != 0)) {
+        atomicOr(&out->rowptr_bad, 1);
+        return;
+    }
+    unsigned long long pc = 0;
+    int beyond = 0, anchor = 0, past = 0;
+    bool unsorted = false;
+    for (int64_t b = s; b < e; ++b) {
+        uint32_t orm = 0;
+        for (int rr = 0; rr < r; ++rr) {
+            const uint32_t m = load_mask(masks, b * r + rr, vs);
+            orm |= m;
+            pc += __popc(m);
+        }
+        if (orm >> vs) beyond = 1;
+        if (!(orm & 1u)) anchor = 1;
+        if (orm && (int64_t)colidx[b] + (31 - __clz(orm)) >= num_cols) past = 1;
+        if (b > s && colidx[b] <= colidx[b - 1]) unsorted = true;
+    }
+    if (pc) atomicAdd(&out->popc, pc);
+    if (beyond) atomicOr(&out->bits_beyond, 1);
+    if (anchor) atomicOr(&out->anchor_missing, 1);
+    if (past) atomicOr(&out->past_end, 1);
+    if (unsorted) atomicMin(&out->first_unsorted_panel, (long long)p);
+}
+
+// ---- chunk plan ----------------------------------------------------------
+// (a) snapped targets
+__global__ void targets_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
+                               int64_t cb, int64_t num_targets, int64_t *cand) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= num_targets) return;
+    if (c == 0) {
+        cand[0] = 0;
+        return;
+    }
+    const int64_t t = c * cb;
+    const int64_t P = upper_bound_dev(rowptr, num_panels, t) - 1;
+    cand[c] = rowptr[P];
+}
+
+// (b) forced splits inside giant panels at global multiples of kSplit
+__device__ __forceinline__ int64_t split_count(int64_t s, int64_t e, int64_t base) {
+    if (e - s <= kSplit) return 0;
+    const int64_t gs = s + base, ge = e + base;
+    // multiples g of kSplit with gs < g < ge
+    const int64_t first = gs / kSplit + 1, last = (ge - 1) / kSplit;
+    return last >= first ? last - first + 1 : 0;
+}
+
+__global__ void split_count_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
+                                   int64_t base, int64_t *counts) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= num_panels) return;
+    counts[p] = split_count(rowptr[p], rowptr[p + 1], base);
+}
+
+__global__ void split_fill_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
+                                  int64_t base, const int64_t *__restrict__ incl, int64_t *out) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= num_panels) return;
+    const int64_t s = rowptr[p], e = rowptr[p + 1];
+    const int64_t n = split_count(s, e, base);
+    if (!n) return;
+    int64_t pos = incl[p] - n;
+    const int64_t first = (s + base) / kSplit + 1;
+    for (int64_t j = 0; j < n; ++j) out[pos + j] = (first + j) * kSplit - base;
+}
+
+__global__ void chunk_desc_kernel(int64_t num_chunks, int64_t num_panels, int r, int vs,
+                                  const int64_t *__restrict__ rowptr, const void *__restrict__ masks,
+                                  const int64_t *__restrict__ tile_prefix,
+                                  const int64_t *__restrict__ chunk_b, int64_t *chunk_v,
+                                  int64_t *chunk_p, uint8_t *split_flag) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < num_chunks; c += nwarps) {
+        const int64_t b = chunk_b[c];
+        const int64_t v = warp_value_offset(b, r, vs, masks, tile_prefix);
+        if (lane == 0) {
+            const int64_t P = upper_bound_dev(rowptr, num_panels, b) - 1;
+            chunk_v[c] = v;
+            chunk_p[c] = P;
+            split_flag[c] = rowptr[P] < b ? 1 : 0;
+        }
+    }
+}
+
+__global__ void empty_flag_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
+                                  uint8_t *flag) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p < num_panels) flag[p] = rowptr[p] == rowptr[p + 1] ? 1 : 0;
+}
+
+// ---- partition_by_nnz ----------------------------------------------------
+__global__ void partition_kernel(int64_t num_panels, int r, int vs,
+                                 const int64_t *__restrict__ rowptr, const void *__restrict__ masks,
+                                 const int64_t *__restrict__ tile_prefix, int64_t num_tiles,
+                                 int workers, int64_t *bounds) {
+    const int lane = threadIdx.x & 31;
+    const int k = (int)((blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5) + 1;
+    if (k >= workers) return;
+    const int64_t total = num_panels ? tile_prefix[num_tiles] : 0;
+    const double target = (double)(total * (int64_t)k) / (double)workers;
+    int64_t res;
+    if (target <= 0) {
+        res = 0;
+    } else {
+        int64_t lo = 0, hi = num_panels;  // searchsorted 'left' over cum[0..num_panels)
+        while (lo < hi) {
+            const int64_t mid = lo + (hi - lo) / 2;
+            const int64_t cum = warp_value_offset(rowptr[mid + 1], r, vs, masks, tile_prefix);
+            if ((double)cum < target) lo = mid + 1;
+            else hi = mid;
+        }
+        res = lo + 1;
+    }
+    if (lane == 0) bounds[k] = res < num_panels ? res : num_panels;
+}
+
+struct BlockPopc {
+    const void *masks;
+    int r, vs;
+    __host__ __device__ int64_t operator()(int64_t b) const {
+#ifdef __CUDA_ARCH__
+        int64_t s = 0;
+        for (int rr = 0; rr < r; ++rr) s += __popc(load_mask(masks, b * r + rr, vs));
+        return s;
+#else
+        return 0;
+#endif
+    }
+};
+
+int select_flagged(const uint8_t *flags, int64_t n, int64_t *out, int64_t *h_count,
+                   cudaStream_t st) {
+    *h_count = 0;
+    if (n <= 0) return SPC5_OK;
+    int64_t *d_count = nullptr;
+    SPC5_TRY(dev_alloc(&d_count, 1));
+    thrust::counting_iterator<int64_t> it(0);
+    size_t bytes = 0;
+    SPC5_CUDA(cub::DeviceSelect::Flagged(nullptr, bytes, it, flags, out, d_count, n, st));
+    void *tmp = nullptr;
+    SPC5_TRY(dev_alloc(&tmp, bytes));
+    SPC5_CUDA(cub::DeviceSelect::Flagged(tmp, bytes, it, flags, out, d_count, n, st));
+    SPC5_CUDA(cudaMemcpyAsync(h_count, d_count, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    dev_free(tmp);
+    dev_free(d_count);
+    return SPC5_OK;
+}
+
+int run_checks(const Matrix &m, CheckOut *h, cudaStream_t st) {
+    CheckOut init{};
+    init.first_unsorted_panel = (long long)INT64_MAX;
+    *h = init;
+    if (m.num_panels == 0) return SPC5_OK;
+    CheckOut *d = nullptr;
+    SPC5_TRY(dev_alloc(&d, 1));
+    SPC5_CUDA(cudaMemcpyAsync(d, &init, sizeof(CheckOut), cudaMemcpyHostToDevice, st));
+    check_kernel<<<(unsigned)cdiv(m.num_panels, 256), 256, 0, st>>>(
+        m.num_panels, m.num_blocks, m.num_cols, m.r, m.vs, m.rowptr, m.colidx, m.masks, d);
+    SPC5_CUDA(cudaGetLastError());
+    SPC5_CUDA(cudaMemcpyAsync(h, d, sizeof(CheckOut), cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    dev_free(d);
+    return SPC5_OK;
+}
+
+int rowptr_ends(const Matrix &m, int64_t *first, int64_t *last, cudaStream_t st) {
+    SPC5_CUDA(cudaMemcpyAsync(first, m.rowptr, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaMemcpyAsync(last, m.rowptr + m.num_panels, sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    return SPC5_OK;
+}
+
+}  // namespace
+
+void free_plan(Plan &p) {
+    dev_free(p.chunk_b);
+    dev_free(p.chunk_v);
+    dev_free(p.chunk_p);
+    dev_free(p.split_chunks);
+    dev_free(p.carry);
+    dev_free(p.empty_panels);
+    dev_free(p.tile_prefix);
+    delete[] p.h_chunk_b;
+    p = Plan{};
+}
+
+int validate_structure(const Matrix &m, cudaStream_t st) {
+    int64_t first = 0, last = 0;
+    SPC5_TRY(rowptr_ends(m, &first, &last, st));
+    CheckOut h;
+    SPC5_TRY(run_checks(m, &h, st));
+    if (h.rowptr_bad || (m.num_panels >= 0 && first != 0))
+        return fail(SPC5_EINVAL, "block_rowptr must be non-decreasing and start at 0");
+    if (m.num_panels && last != m.num_blocks)
+        return fail(SPC5_EINVAL, "block_rowptr does not cover all blocks");
+    if (h.bits_beyond) return fail(SPC5_EINVAL, "mask has bits beyond vs");
+    if ((int64_t)h.popc != m.nnz) return fail(SPC5_EINVAL, "sum of mask popcounts differs from NNZ");
+    if (m.num_blocks) {
+        if (h.anchor_missing) return fail(SPC5_EINVAL, "block without an entry at its anchor column");
+        if (h.first_unsorted_panel != (long long)INT64_MAX)
+            return fail(SPC5_EINVAL, "panel " + std::to_string(h.first_unsorted_panel) +
+                                         ": block columns not strictly increasing");
+        if (h.past_end) return fail(SPC5_EINVAL, "set mask bit maps past the last column");
+    }
+    return SPC5_OK;
+}
+
+int build_plan(Matrix &m, bool validate, cudaStream_t st) {
+    if (m.plan.built) return SPC5_OK;
+    Plan &P = m.plan;
+    const int64_t nb = m.num_blocks, np = m.num_panels;
+    if (validate) {
+        // the checks the reference kernels perform implicitly
+        int64_t first = 0, last = 0;
+        SPC5_TRY(rowptr_ends(m, &first, &last, st));
+        CheckOut h;
+        SPC5_TRY(run_checks(m, &h, st));
+        if (h.rowptr_bad || first != 0 || last != nb)
+            return fail(SPC5_EINVAL, "block_rowptr must be non-decreasing from 0 to num_blocks");
+        if (h.bits_beyond) return fail(SPC5_EINVAL, "mask has bits beyond the vs lanes");
+        if ((int64_t)h.popc != m.nnz)
+            return fail(SPC5_ECURSOR, "value cursor ended at " + std::to_string(h.popc) +
+                                          ", expected " + std::to_string(m.nnz));
+        if (h.past_end)
+            return fail(SPC5_EINDEX, "active lane past end of x (mask bit maps past the last column)");
+    }
+    // popcount prefix per tile
+    P.num_tiles = cdiv(nb, kTile);
+    SPC5_TRY(dev_alloc(&P.tile_prefix, (size_t)P.num_tiles + 1));
+    SPC5_CUDA(cudaMemsetAsync(P.tile_prefix, 0, sizeof(int64_t) * (P.num_tiles + 1), st));
+    if (P.num_tiles) {
+        int64_t *sums = nullptr;
+        SPC5_TRY(dev_alloc(&sums, (size_t)P.num_tiles));
+        tile_sums_kernel<<<(unsigned)std::min<int64_t>(cdiv(P.num_tiles, 8), 148 * 32), 256, 0,
+                           st>>>(nb, m.r, m.vs, m.masks, P.num_tiles, sums);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_TRY(scan_inclusive_i64(sums, P.tile_prefix + 1, P.num_tiles, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(sums);
+    }
+    // empty panels (zeroed by the SpMV kernel in y = A.x mode)
+    if (np) {
+        uint8_t *flags = nullptr;
+        SPC5_TRY(dev_alloc(&flags, (size_t)np));
+        empty_flag_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, flags);
+        SPC5_TRY(dev_alloc(&P.empty_panels, (size_t)np));
+        SPC5_TRY(select_flagged(flags, np, P.empty_panels, &P.num_empty, st));
+        dev_free(flags);
+    }
+    if (nb == 0) {
+        P.num_chunks = 0;
+        P.h_chunk_b = new int64_t[1]{0};
+        P.built = true;
+        return SPC5_OK;
+    }
+    // chunk granularity: ~4 chunks per resident warp, multiple of 32, [32, 1024]
+    const int64_t resident_warps = (int64_t)m.sm_count * 32;
+    int64_t cb = cdiv(nb, resident_warps * 4);
+    cb = std::max<int64_t>(32, std::min<int64_t>(1024, cdiv(cb, 32) * 32));
+    const int64_t num_targets = cdiv(nb, cb);
+    int64_t *split_counts = nullptr;
+    SPC5_TRY(dev_alloc(&split_counts, (size_t)np));
+    split_count_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
+                                                                 split_counts);
+    int64_t *split_incl = nullptr;
+    SPC5_TRY(dev_alloc(&split_incl, (size_t)np));
+    SPC5_TRY(scan_inclusive_i64(split_counts, split_incl, np, st));
+    int64_t num_forced = 0;
+    SPC5_CUDA(cudaMemcpyAsync(&num_forced, split_incl + np - 1, sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    const int64_t ncand = num_targets + num_forced;
+    int64_t *cand = nullptr, *sorted = nullptr;
+    SPC5_TRY(dev_alloc(&cand, (size_t)ncand));
+    SPC5_TRY(dev_alloc(&sorted, (size_t)ncand + 1));
+    targets_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(np, m.rowptr, cb,
+                                                                      num_targets, cand);
+    if (num_forced)
+        split_fill_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
+                                                                    split_incl,
+                                                                    cand + num_targets);
+    SPC5_CUDA(cudaGetLastError());
+    {
+        size_t bytes = 0;
+        SPC5_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, cand, sorted, ncand, 0, 64, st));
+        void *tmp = nullptr;
+        SPC5_TRY(dev_alloc(&tmp, bytes));
+        SPC5_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, cand, sorted, ncand, 0, 64, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(tmp);
+    }
+    int64_t *d_nuniq = nullptr;
+    SPC5_TRY(dev_alloc(&d_nuniq, 1));
+    SPC5_TRY(dev_alloc(&P.chunk_b, (size_t)ncand + 1));
+    {
+        size_t bytes = 0;
+        SPC5_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, sorted, P.chunk_b, d_nuniq, ncand, st));
+        void *tmp = nullptr;
+        SPC5_TRY(dev_alloc(&tmp, bytes));
+        SPC5_CUDA(cub::DeviceSelect::Unique(tmp, bytes, sorted, P.chunk_b, d_nuniq, ncand, st));
+        SPC5_CUDA(cudaMemcpyAsync(&P.num_chunks, d_nuniq, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(tmp);
+    }
+    dev_free(d_nuniq);
+    dev_free(cand);
+    dev_free(sorted);
+    dev_free(split_counts);
+    dev_free(split_incl);
+    const int64_t nc = P.num_chunks;
+    SPC5_CUDA(cudaMemcpyAsync(P.chunk_b + nc, &nb, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    SPC5_TRY(dev_alloc(&P.chunk_v, (size_t)nc));
+    SPC5_TRY(dev_alloc(&P.chunk_p, (size_t)nc));
+    uint8_t *split_flag = nullptr;
+    SPC5_TRY(dev_alloc(&split_flag, (size_t)nc));
+    chunk_desc_kernel<<<(unsigned)std::min<int64_t>(cdiv(nc, 8), 148 * 32), 256, 0, st>>>(
+        nc, np, m.r, m.vs, m.rowptr, m.masks, P.tile_prefix, P.chunk_b, P.chunk_v, P.chunk_p,
+        split_flag);
+    SPC5_CUDA(cudaGetLastError());
+    SPC5_TRY(dev_alloc(&P.split_chunks, (size_t)nc));
+    SPC5_TRY(select_flagged(split_flag, nc, P.split_chunks, &P.num_split, st));
+    dev_free(split_flag);
+    if (P.num_split) SPC5_TRY(dev_alloc(&P.carry, (size_t)nc * m.r));
+    P.h_chunk_b = new int64_t[nc + 1];
+    SPC5_CUDA(cudaMemcpyAsync(P.h_chunk_b, P.chunk_b, sizeof(int64_t) * (nc + 1),
+                              cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    P.built = true;
+    return SPC5_OK;
+}
+
+int partition_by_nnz(const Matrix &m, int workers, int64_t *h_ranges, cudaStream_t st) {
+    if (workers < 1) return fail(SPC5_EINVAL, "workers must be >= 1");
+    std::vector<int64_t> bounds(workers + 1, 0);
+    bounds[workers] = m.num_panels;
+    if (workers > 1 && m.num_panels > 0) {
+        int64_t *d = nullptr;
+        SPC5_TRY(dev_alloc(&d, (size_t)workers + 1));
+        const int64_t threads = (int64_t)(workers - 1) * 32;
+        partition_kernel<<<(unsigned)cdiv(threads, 128), 128, 0, st>>>(
+            m.num_panels, m.r, m.vs, m.rowptr, m.masks, m.plan.tile_prefix, m.plan.num_tiles,
+            workers, d);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_CUDA(cudaMemcpyAsync(bounds.data() + 1, d + 1, sizeof(int64_t) * (workers - 1),
+                                  cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(d);
+    }
+    for (int k = 0; k < workers; ++k) {
+        h_ranges[2 * k] = bounds[k];
+        h_ranges[2 * k + 1] = bounds[k + 1];
+    }
+    note_launches(workers > 1 && m.num_panels > 0 ? 1 : 0);
+    return SPC5_OK;
+}
+
+int block_value_offsets(const Matrix &m, int64_t *d_offsets, cudaStream_t st) {
+    SPC5_CUDA(cudaMemsetAsync(d_offsets, 0, sizeof(int64_t), st));
+    if (m.num_blocks == 0) return SPC5_OK;
+    BlockPopc f{m.masks, m.r, m.vs};
+    thrust::transform_iterator<BlockPopc, thrust::counting_iterator<int64_t>> it(
+        thrust::counting_iterator<int64_t>(0), f);
+    size_t bytes = 0;
+    SPC5_CUDA(cub::DeviceScan::InclusiveSum(nullptr, bytes, it, d_offsets + 1, m.num_blocks, st));
+    void *tmp = nullptr;
+    SPC5_TRY(dev_alloc(&tmp, bytes));
+    SPC5_CUDA(cub::DeviceScan::InclusiveSum(tmp, bytes, it, d_offsets + 1, m.num_blocks, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    dev_free(tmp);
+    return SPC5_OK;
+}
+
+}  // namespace spc5
