@@ -53,39 +53,6 @@ __device__ __forceinline__ uint32_t ldg_nc_u32(const uint32_t *p) {
     return v;
 }
 
-template <int BYTES>
-struct MaskWords {
-    static constexpr int N = (BYTES + 3) / 4;
-    uint32_t w[N];
-    __device__ __forceinline__ void load(const uint8_t *p) {
-        if constexpr (BYTES == 1) {
-            w[0] = *p;
-        } else if constexpr (BYTES == 2) {
-            w[0] = *reinterpret_cast<const uint16_t *>(p);
-        } else if constexpr (BYTES == 4) {
-            w[0] = ldg_nc_u32(reinterpret_cast<const uint32_t *>(p));
-        } else if constexpr (BYTES == 8) {
-            uint2 v;
-            asm volatile("ld.global.nc.L1::no_allocate.v2.u32 {%0, %1}, [%2];"
-                         : "=r"(v.x), "=r"(v.y) : "l"(p));
-            w[0] = v.x;
-            w[1] = v.y;
-        } else {
-            uint4 v;
-            asm volatile("ld.global.nc.L1::no_allocate.v4.u32 {%0, %1, %2, %3}, [%4];"
-                         : "=r"(v.x), "=r"(v.y), "=r"(v.z), "=r"(v.w) : "l"(p));
-            w[0] = v.x;
-            w[1] = v.y;
-            w[2] = v.z;
-            w[3] = v.w;
-        }
-    }
-    __device__ __forceinline__ void zero() {
-#pragma unroll
-        for (int i = 0; i < N; ++i) w[i] = 0;
-    }
-};
-
 template <typename T>
 __device__ __forceinline__ double mul_acc(double acc, T v, T xv);
 template <>
@@ -99,16 +66,60 @@ __device__ __forceinline__ double mul_acc<float>(double acc, float v, float xv) 
 
 constexpr unsigned kFull = 0xffffffffu;
 
-template <typename T, typename MT, int R>
-__global__ void __launch_bounds__(256) spmv_kernel(const SpmvArgs a) {
+template <int BYTES>
+__device__ __forceinline__ uint32_t load_lane_mask(const uint8_t *p) {
+    if constexpr (BYTES == 1) {
+        return *p;
+    } else if constexpr (BYTES == 2) {
+        return *reinterpret_cast<const uint16_t *>(p);
+    } else {
+        return ldg_nc_u32(reinterpret_cast<const uint32_t *>(p));
+    }
+}
+
+// Window state: one lane = G consecutive rows of one block.
+struct WinState {
+    uint32_t col;  // block column start
+    uint32_t fm;   // the lane's G masks, concatenated (row g at bits [g*MBITS, ...))
+    int64_t E;     // block_rowptr[pc + 1 + lane]: end of panel pc + lane
+};
+
+// Exclusive prefix sum over the warp of a small count (< 2^NP) via bit-plane
+// ballots: independent BALLOT/POPC pairs instead of a dependent shuffle chain.
+template <int NP>
+__device__ __forceinline__ void warp_prefix(int cnt, int lane, int &excl, int &total) {
+    const unsigned lt = (1u << lane) - 1u;
+    excl = 0;
+    total = 0;
+#pragma unroll
+    for (int p = 0; p < NP; ++p) {
+        const unsigned bal = __ballot_sync(kFull, (cnt >> p) & 1);
+        excl += __popc(bal & lt) << p;
+        total += __popc(bal) << p;
+    }
+}
+
+// K2.  R rows per panel, G rows per lane, L = R/G lanes per block,
+// BW = 32/L blocks per window (windows aligned to global multiples of BW).
+template <typename T, typename MT, int R, int G>
+__global__ void __launch_bounds__(256, 3) spmv_kernel(const SpmvArgs a) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int MBITS = 8 * MB;
+    constexpr int L = R / G;
+    constexpr int BW = 32 / L;
+    constexpr int LB = G * MB;  // mask bytes per lane
+    static_assert(LB <= 4, "a lane's masks must fit 32 bits");
+    constexpr int NP = (G * MBITS >= 32) ? 6 : (G * MBITS >= 16 ? 5 : 4);
+    constexpr int NB = 4;  // value slots per batch
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
+    const int blk = lane / L;
+    const int sub = lane % L;
     const T *__restrict__ vals = static_cast<const T *>(a.values);
     const T *__restrict__ x = static_cast<const T *>(a.x);
     T *__restrict__ y = static_cast<T *>(a.y);
     const int64_t *__restrict__ rowptr = a.rowptr;
+    const uint8_t *__restrict__ masks = static_cast<const uint8_t *>(a.masks);
 
     if (!a.accumulate) {  // y = A.x: rows of empty panels are zero
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.num_empty;
@@ -122,155 +133,186 @@ __global__ void __launch_bounds__(256) spmv_kernel(const SpmvArgs a) {
     }
 
     const int64_t nc = a.c_hi - a.c_lo;
-    for (int64_t g = blockIdx.x; g * kWarpsPerCta < nc; g += gridDim.x) {
-        const int64_t c = a.c_lo + g * kWarpsPerCta + warp;
+    for (int64_t gi = blockIdx.x; gi * kWarpsPerCta < nc; gi += gridDim.x) {
+        const int64_t c = a.c_lo + gi * kWarpsPerCta + warp;
         if (c >= a.c_hi) break;
         const int64_t cb0 = a.chunk_b[c], cb1 = a.chunk_b[c + 1];
         const int64_t b0 = max(cb0, a.b_lo), b1 = min(cb1, a.b_hi);
         if (b0 >= b1) continue;
-        int64_t v = a.chunk_v[c];
-        int64_t pc = a.chunk_p[c];
-        int64_t ps = __ldg(rowptr + pc);
-        double carry[R];
+        const int64_t p0 = a.chunk_p[c];
+        const bool head_mid = __ldg(rowptr + p0) < cb0;  // chunk starts inside panel p0
+        const T *__restrict__ vbase = vals + a.chunk_v[c];
+        uint32_t vrel = 0;  // value cursor relative to the chunk
+        int64_t pc = p0;
+        int64_t wb = cb0 - ((cb0 + a.base_mod) % BW);
+
+        auto load_win = [&](int64_t w, int64_t pcw, WinState &st) {
+            const int64_t b = w + blk;
+            st.col = 0;
+            st.fm = 0;
+            if (b >= cb0 && b < b1) {
+                st.col = ldg_nc_u32(a.colidx + b);
+                st.fm = load_lane_mask<LB>(masks + (b * R + sub * G) * MB);
+            }
+            const int64_t e = pcw + 1 + lane;
+            st.E = e <= a.num_panels ? __ldg(rowptr + e) : INT64_MAX;
+        };
+        WinState cur, nxt;
+        load_win(wb, pc, cur);
+
+        double carry[G];
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) carry[rr] = 0.0;
+        for (int g = 0; g < G; ++g) carry[g] = 0.0;
         int64_t carry_panel = -1;
-        const int64_t w0 = cb0 - ((cb0 + a.base_mod) & 31);
-        for (int64_t w = w0; w < b1; w += 32) {
-            const int64_t b = w + lane;
-            const bool counted = b >= cb0 && b < b1;  // contributes to the value cursor
-            const bool act = b >= b0 && b < b1;       // contributes to y
-            uint32_t col = 0;
-            MaskWords<R * MB> mw;
-            mw.zero();
-            if (counted) {
-                col = ldg_nc_u32(a.colidx + b);
-                mw.load(static_cast<const uint8_t *>(a.masks) + b * (R * MB));
-            }
-            int cnt = 0;
-#pragma unroll
-            for (int i = 0; i < MaskWords<R * MB>::N; ++i) cnt += __popc(mw.w[i]);
-            int incl = cnt;
-#pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-                const int t = __shfl_up_sync(kFull, incl, d);
-                if (lane >= d) incl += t;
-            }
-            int64_t off = v + incl - cnt;
-            v += __shfl_sync(kFull, incl, 31);
 
-            // ---- panel of the lane's block
-            const int64_t bq = min(max(b, cb0), b1 - 1);
-            const int64_t eidx = pc + 1 + lane;
-            const int64_t E = eidx <= a.num_panels ? __ldg(rowptr + eidx) : INT64_MAX;
-            int cp = 0;
-#pragma unroll
-            for (int s = 16; s >= 1; s >>= 1) {
-                const int64_t e = __shfl_sync(kFull, E, cp + s - 1);
-                if (e <= bq) cp += s;
-            }
-            const int64_t e31 = __shfl_sync(kFull, E, 31);
-            const int64_t e_lo = __shfl_sync(kFull, E, cp > 0 ? cp - 1 : 0);
-            const int64_t e_hi = __shfl_sync(kFull, E, cp);
-            int64_t pl = pc + cp;
-            int64_t pstart = cp ? e_lo : ps;
-            int64_t pend = e_hi;
-            const bool ovf = (cp == 31) && (e31 <= bq);
-            if (__any_sync(kFull, ovf) && ovf) {
-                int64_t lo = pc, hi = a.num_panels;  // last p with rowptr[p] <= bq
-                while (lo < hi) {
-                    const int64_t mid = lo + (hi - lo + 1) / 2;
-                    if (__ldg(rowptr + mid) <= bq) lo = mid;
-                    else hi = mid - 1;
-                }
-                pl = lo;
-                pstart = __ldg(rowptr + pl);
-                pend = __ldg(rowptr + pl + 1);
-            }
-            // lanes past the chunk (or range) end form their own segment: appending
-            // zero lanes to the last panel's segment would change its sum's association
-            if (b >= b1) pl = INT64_MAX;
-
-            // ---- the block's dot products (one per panel row)
-            double acc[R];
-#pragma unroll
-            for (int rr = 0; rr < R; ++rr) {
-                uint32_t mm = (mw.w[(rr * MB) / 4] >> (((rr * MB) % 4) * 8)) &
-                              (MBITS == 32 ? 0xffffffffu : ((1u << MBITS) - 1u));
-                double s = 0.0;
-                if (act) {
-                    while (mm) {
-                        const int k = __ffs(mm) - 1;
-                        mm &= mm - 1;
-                        s = mul_acc<T>(s, __ldg(vals + off), __ldg(x + col + k));
-                        ++off;
+        for (;;) {
+            const int64_t wn = wb + BW;
+            const bool last = wn >= b1;
+            // ---- panel containing the next window's first block, then prefetch it
+            int64_t pcn = pc;
+            if (!last) {
+                const int cn = __popc(__ballot_sync(kFull, cur.E <= wn));
+                if (cn < 32) {
+                    pcn = pc + cn;
+                } else {
+                    int64_t lo = pc, hi = a.num_panels;
+                    while (lo < hi) {
+                        const int64_t mid = lo + (hi - lo + 1) / 2;
+                        if (__ldg(rowptr + mid) <= wn) lo = mid;
+                        else hi = mid - 1;
                     }
-                } else {
-                    off += __popc(mm);
+                    pcn = lo;
                 }
-                acc[rr] = s;
-            }
-            if (lane == 0 && pl == carry_panel) {
-#pragma unroll
-                for (int rr = 0; rr < R; ++rr) acc[rr] += carry[rr];
+                load_win(wn, pcn, nxt);
             }
 
-            // ---- segmented reduction over lanes of the same panel
-            const int64_t pl_prev = __shfl_up_sync(kFull, pl, 1);
-            const bool head = lane == 0 || pl != pl_prev;
-            const unsigned heads = __ballot_sync(kFull, head);
-            const unsigned le = heads & (kFull >> (31 - lane));
-            const int segstart = 31 - __clz(le);
+            // ---- value offsets
+            const int64_t b = wb + blk;
+            const bool act = b >= b0 && b < b1;
+            const int cnt = __popc(cur.fm);
+            int excl, total;
+            warp_prefix<NP>(cnt, lane, excl, total);
+
+            // ---- panel of each block (block-level start bits)
+            const int64_t d = cur.E - wb;
+            const bool in = d >= 1 && d < BW;
+            unsigned starts = __reduce_or_sync(kFull, in ? (1u << (int)d) : 0u);
+            const int nin = __popc(__ballot_sync(kFull, in));
+            int64_t pl, pend_last;
+            const unsigned blk_le = (BW == 32 && blk == 31) ? kFull : ((2u << blk) - 1u);
+            if (__popc(starts) == nin) {  // no empty panel inside the window
+                pl = pc + __popc(starts & blk_le);
+                pend_last = __shfl_sync(kFull, cur.E, __popc(starts));
+            } else {  // empty panels: per-lane search over the loaded ends
+                const int64_t bq = max(b, cb0);
+                int cp = 0;
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
+                for (int s = 16; s >= 1; s >>= 1) {
+                    const int64_t e = __shfl_sync(kFull, cur.E, cp + s - 1);
+                    if (e <= bq) cp += s;
+                }
+                const int64_t e31 = __shfl_sync(kFull, cur.E, 31);
+                pl = pc + cp;
+                if (cp == 31 && e31 <= bq) {
+                    int64_t lo = pc, hi = a.num_panels;
+                    while (lo < hi) {
+                        const int64_t mid = lo + (hi - lo + 1) / 2;
+                        if (__ldg(rowptr + mid) <= bq) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    pl = lo;
+                }
+                const int64_t pprev = __shfl_up_sync(kFull, pl, L);
+                const unsigned hb = __ballot_sync(kFull, sub == 0 && blk > 0 && pl != pprev);
+                starts = 0;
 #pragma unroll
-                for (int rr = 0; rr < R; ++rr) {
-                    const double t = __shfl_up_sync(kFull, acc[rr], d);
-                    if (lane - d >= segstart) acc[rr] += t;
+                for (int t = 1; t < BW; ++t) starts |= ((hb >> (t * L)) & 1u) << t;
+                const int64_t pl_last = __shfl_sync(kFull, pl, 31);
+                pend_last = __ldg(rowptr + pl_last + 1);
+            }
+            // blocks past the chunk/range end: their own (silent) segment
+            if (b1 - wb < BW) starts |= 1u << (int)(b1 - wb);
+            const unsigned hbits = starts | 1u;
+
+            // ---- the lane's rows of its block: batched loads, then FMAs
+            double acc[G];
+#pragma unroll
+            for (int g = 0; g < G; ++g) acc[g] = 0.0;
+            const int cmax = __reduce_max_sync(kFull, act ? cnt : 0);
+            if (cmax > 0) {
+                const T *__restrict__ vp = vbase + (vrel + (uint32_t)excl);
+                const T *__restrict__ xp = x + cur.col;
+                uint32_t fmc = act ? cur.fm : 0u;
+                for (int j0 = 0; j0 < cmax; j0 += NB) {
+                    T vv[NB], xv[NB];
+                    int gsel[NB];
+#pragma unroll
+                    for (int u = 0; u < NB; ++u) {
+                        const bool valid = fmc != 0u;
+                        const int pos = __ffs(fmc) - 1;
+                        fmc &= fmc - 1u;
+                        gsel[u] = valid ? (G == 1 ? 0 : pos / MBITS) : -1;
+                        const int k = pos & (MBITS - 1);
+                        vv[u] = valid ? __ldg(vp + j0 + u) : T(0);
+                        xv[u] = valid ? __ldg(xp + k) : T(0);
+                    }
+#pragma unroll
+                    for (int u = 0; u < NB; ++u) {
+                        if (G == 1) {
+                            if (gsel[u] == 0) acc[0] = mul_acc<T>(acc[0], vv[u], xv[u]);
+                        } else {
+                            // every accumulator is written (a zero where the row differs)
+                            // so the compiler keeps acc[] in registers
+                            const double p = mul_acc<T>(0.0, vv[u], xv[u]);
+#pragma unroll
+                            for (int g = 0; g < G; ++g) acc[g] += (gsel[u] == g) ? p : 0.0;
+                        }
+                    }
                 }
             }
-            const bool tail = lane == 31 || ((heads >> (lane + 1)) & 1u);
-            const bool last_window = w + 32 >= b1;
-            const bool cont = pend > w + 32;
-            if (tail && !(cont && !last_window) && pl >= a.p_lo && pl < a.p_hi) {
-                if (pstart < cb0) {
+            vrel += (uint32_t)total;
+            if (blk == 0 && pl == carry_panel) {
 #pragma unroll
-                    for (int rr = 0; rr < R; ++rr) a.carry[c * R + rr] = acc[rr];
+                for (int g = 0; g < G; ++g) acc[g] += carry[g];
+            }
+
+            // ---- segmented scan over blocks of the same panel (stride L lanes)
+            const int segstart = 31 - __clz(hbits & blk_le);
+#pragma unroll
+            for (int dd = 1; dd < BW; dd <<= 1) {
+#pragma unroll
+                for (int g = 0; g < G; ++g) {
+                    const double t = __shfl_up_sync(kFull, acc[g], dd * L);
+                    if (blk - dd >= segstart) acc[g] += t;
+                }
+            }
+            const bool tailb = blk == BW - 1 || ((hbits >> (blk + 1)) & 1u);
+            const bool cont = pend_last > wn;  // last block's panel continues past the window
+            if (tailb && act && !(blk == BW - 1 && cont && !last) && pl >= a.p_lo &&
+                pl < a.p_hi) {
+                if (head_mid && pl == p0) {
+#pragma unroll
+                    for (int g = 0; g < G; ++g) a.carry[c * R + sub * G + g] = acc[g];
                 } else {
 #pragma unroll
-                    for (int rr = 0; rr < R; ++rr) {
-                        const int64_t row = pl * R + rr;
+                    for (int g = 0; g < G; ++g) {
+                        const int64_t row = pl * R + sub * G + g;
                         if (row < a.num_rows) {
-                            const T sv = (T)acc[rr];
+                            const T sv = (T)acc[g];
                             y[row] = a.accumulate ? y[row] + sv : sv;
                         }
                     }
                 }
             }
-            if (last_window) break;
-            // ---- state for the next window
-            const bool c31 = __shfl_sync(kFull, cont, 31);
-            const int64_t pl31 = __shfl_sync(kFull, pl, 31);
+            if (last) break;
+            // ---- carry into the next window
+            const int64_t pl_last = __shfl_sync(kFull, pl, 31);
 #pragma unroll
-            for (int rr = 0; rr < R; ++rr) carry[rr] = __shfl_sync(kFull, acc[rr], 31);
-            carry_panel = c31 ? pl31 : -1;
-            const int64_t bn = w + 32;
-            const unsigned le_bn = __ballot_sync(kFull, E <= bn);
-            const int cn = __popc(le_bn);
-            if (cn < 32) {
-                const int64_t e_prev = __shfl_sync(kFull, E, cn > 0 ? cn - 1 : 0);
-                ps = cn ? e_prev : ps;
-                pc = pc + cn;
-            } else {
-                int64_t lo = pc, hi = a.num_panels;
-                while (lo < hi) {
-                    const int64_t mid = lo + (hi - lo + 1) / 2;
-                    if (__ldg(rowptr + mid) <= bn) lo = mid;
-                    else hi = mid - 1;
-                }
-                pc = lo;
-                ps = __ldg(rowptr + pc);
-            }
+            for (int g = 0; g < G; ++g) carry[g] = __shfl_sync(kFull, acc[g], (BW - 1) * L + sub);
+            carry_panel = cont ? pl_last : -1;
+            pc = pcn;
+            wb = wn;
+            cur = nxt;
         }
     }
 }
@@ -303,12 +345,12 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
     }
 }
 
-template <typename T, typename MT, int R>
+template <typename T, typename MT, int R, int G>
 int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
     static int max_blocks_per_sm = 0;
     if (!max_blocks_per_sm) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm, spmv_kernel<T, MT, R>,
-                                                      256, 0);
+        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm,
+                                                      spmv_kernel<T, MT, R, G>, 256, 0);
         if (max_blocks_per_sm < 1) max_blocks_per_sm = 1;
     }
     const int64_t nc = a.c_hi - a.c_lo;
@@ -316,7 +358,7 @@ int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
                                      a.accumulate ? 1 : cdiv(a.num_empty, 256));
     grid = std::min<int64_t>(grid, (int64_t)m.sm_count * max_blocks_per_sm);
     grid = std::max<int64_t>(grid, 1);
-    spmv_kernel<T, MT, R><<<(unsigned)grid, 256, 0, st>>>(a);
+    spmv_kernel<T, MT, R, G><<<(unsigned)grid, 256, 0, st>>>(a);
     SPC5_CUDA(cudaGetLastError());
     int launches = 1;
     if (m.plan.num_split) {
@@ -332,11 +374,14 @@ int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
 
 template <typename T, typename MT>
 int dispatch_r(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
+    // G rows per lane: a lane's masks must fit 32 bits (G*sizeof(MT) <= 4)
+    constexpr int G2 = sizeof(MT) == 1 ? 2 : 2;
+    constexpr int G4 = sizeof(MT) == 1 ? 4 : 2;
     switch (m.r) {
-        case 1: return launch_typed<T, MT, 1>(m, a, st);
-        case 2: return launch_typed<T, MT, 2>(m, a, st);
-        case 4: return launch_typed<T, MT, 4>(m, a, st);
-        default: return launch_typed<T, MT, 8>(m, a, st);
+        case 1: return launch_typed<T, MT, 1, 1>(m, a, st);
+        case 2: return launch_typed<T, MT, 2, G2>(m, a, st);
+        case 4: return launch_typed<T, MT, 4, G4>(m, a, st);
+        default: return launch_typed<T, MT, 8, G4>(m, a, st);
     }
 }
 
@@ -360,7 +405,7 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
     a.carry = P.carry;
     a.empty_panels = P.empty_panels;
     a.num_empty = P.num_empty;
-    a.base_mod = (int)(((m.block_base % 32) + 32) % 32);
+    a.base_mod = (int)(((m.block_base % 32) + 32) % 32);  // windows divide 32
     a.accumulate = accumulate;
     a.p_lo = p_lo;
     a.p_hi = p_hi;
