@@ -25,8 +25,8 @@ struct Plan {
     bool built = false;
     int64_t num_chunks = 0;
     int64_t *chunk_b = nullptr;  // [num_chunks+1] first block of each chunk (+ nb)
-    int64_t *chunk_v = nullptr;  // [num_chunks]   value offset of that block
-    int64_t *chunk_p = nullptr;  // [num_chunks]   panel containing that block
+    int64_t *chunk_v = nullptr;  // [num_chunks+1] value offset of that block (+ nnz)
+    int64_t *chunk_p = nullptr;  // [num_chunks+1] panel containing that block (+ num_panels)
     int64_t *h_chunk_b = nullptr;  // host copy of chunk_b (range launches)
     int64_t num_split = 0;       // chunks whose first block is inside a panel
     int64_t *split_chunks = nullptr;  // [num_split] their indices, ascending
@@ -35,6 +35,15 @@ struct Plan {
     int64_t *empty_panels = nullptr;  // [num_empty] panels with no block
     int64_t num_tiles = 0;
     int64_t *tile_prefix = nullptr;   // [num_tiles+1] value offset at tile starts
+    // TMA stages: groups of `stage_granules` 32-block granules aligned to global
+    // multiples of 32 blocks (so no warp window straddles two stages)
+    int stage_granules = 1;
+    int64_t num_stages = 0;
+    int64_t *stage_v = nullptr;  // [num_stages+1] value offset at stage starts (+ nnz)
+    int64_t *stage_p = nullptr;  // [num_stages+1] panel containing the stage start (+ num_panels)
+    int64_t stage_vmax = 0;      // max values in one stage
+    int rp_cap = 0;              // rowptr entries staged per stage (else read from global)
+    int slot_bytes = 0;          // smem bytes of one stage slot
 };
 
 struct Matrix {

@@ -66,6 +66,8 @@ __device__ __forceinline__ int64_t upper_bound_dev(const int64_t *a, int64_t n, 
     return lo;
 }
 
+__device__ __forceinline__ int64_t cdiv_dev(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
 // structural checks over panels (thread per panel)
 struct CheckOut {
     unsigned long long popc;
@@ -178,6 +180,67 @@ __global__ void empty_flag_kernel(int64_t num_panels, const int64_t *__restrict_
     if (p < num_panels) flag[p] = rowptr[p] == rowptr[p + 1] ? 1 : 0;
 }
 
+// ---- TMA stage plan ---------------------------------------------------------
+// Granule g covers local blocks [gstart(g), gstart(g+1)) with
+// gstart(g) = max(0, 32*g - off32), off32 = block_base mod 32: granule
+// boundaries are global multiples of 32 blocks.
+__device__ __forceinline__ int64_t granule_start(int64_t g, int64_t ng, int64_t nb, int off32) {
+    if (g <= 0) return 0;
+    if (g >= ng) return nb;
+    const int64_t b = g * 32 - off32;
+    return b < nb ? b : nb;
+}
+
+__global__ void granule_sums_kernel(int64_t nb, int r, int vs, const void *__restrict__ masks,
+                                    int off32, int64_t ng, int *gsum) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t g = warp; g < ng; g += nwarps) {
+        const int64_t lo = granule_start(g, ng, nb, off32), hi = granule_start(g + 1, ng, nb, off32);
+        int s = 0;
+        const int64_t b = lo + lane;
+        if (b < hi)
+            for (int rr = 0; rr < r; ++rr) s += __popc(load_mask(masks, b * r + rr, vs));
+        s = __reduce_add_sync(0xffffffffu, s);
+        if (lane == 0) gsum[g] = s;
+    }
+}
+
+// per candidate stage size k (granules): max values and max staged rowptr entries
+__global__ void stage_stats_kernel(int64_t ng, int k, const int *__restrict__ gsum, int64_t nb,
+                                   int off32, const int64_t *__restrict__ rowptr, int64_t np,
+                                   unsigned long long *vmax, unsigned long long *pmax) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t ns = cdiv_dev(ng, k);
+    if (j >= ns) return;
+    long long s = 0;
+    for (int64_t g = j * k; g < min((j + 1) * k, ng); ++g) s += gsum[g];
+    atomicMax(vmax, (unsigned long long)s);
+    const int64_t b0 = granule_start(j * k, ng, nb, off32);
+    const int64_t b1 = granule_start((j + 1) * k, ng, nb, off32);
+    const int64_t p0 = upper_bound_dev(rowptr, np, b0) - 1;
+    const int64_t p1 = b1 < nb ? upper_bound_dev(rowptr, np, b1) - 1 : np;
+    const int64_t cnt = min(p1 + 1, np) - p0 + 1;
+    atomicMax(pmax, (unsigned long long)cnt);
+}
+
+__global__ void stage_fill_kernel(int64_t ng, int k, const int *__restrict__ gsum, int64_t nb,
+                                  int off32, const int64_t *__restrict__ rowptr, int64_t np,
+                                  int64_t ns, int64_t *stage_sum, int64_t *stage_p) {
+    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (j > ns) return;
+    if (j == ns) {
+        stage_p[j] = np;
+        return;
+    }
+    long long s = 0;
+    for (int64_t g = j * k; g < min((j + 1) * k, ng); ++g) s += gsum[g];
+    stage_sum[j] = s;
+    const int64_t b0 = granule_start(j * k, ng, nb, off32);
+    stage_p[j] = upper_bound_dev(rowptr, np, b0) - 1;
+}
+
 // ---- partition_by_nnz ----------------------------------------------------
 __global__ void partition_kernel(int64_t num_panels, int r, int vs,
                                  const int64_t *__restrict__ rowptr, const void *__restrict__ masks,
@@ -272,6 +335,8 @@ void free_plan(Plan &p) {
     dev_free(p.carry);
     dev_free(p.empty_panels);
     dev_free(p.tile_prefix);
+    dev_free(p.stage_v);
+    dev_free(p.stage_p);
     delete[] p.h_chunk_b;
     p = Plan{};
 }
@@ -294,6 +359,69 @@ int validate_structure(const Matrix &m, cudaStream_t st) {
                                          ": block columns not strictly increasing");
         if (h.past_end) return fail(SPC5_EINVAL, "set mask bit maps past the last column");
     }
+    return SPC5_OK;
+}
+
+// Stage size: the largest power-of-two number of granules whose worst stage
+// (values + headers + staged rowptr) fits kSlotTarget bytes of shared memory.
+static int slot_bytes_for(int64_t sb, int64_t vmax, int64_t rp_cap, int r, int mb, int vb) {
+    auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
+    // +32 per region: a bulk copy is widened to 16-byte alignment at both ends
+    const int64_t bytes = a16(sb * 4 + 32) + a16(sb * r * mb + 32) + a16(rp_cap * 8 + 32) +
+                          a16(vmax * vb + 32);
+    return (int)((bytes + 127) / 128 * 128);
+}
+
+int build_stages(Matrix &m, cudaStream_t st) {
+    Plan &P = m.plan;
+    const int64_t nb = m.num_blocks, np = m.num_panels;
+    const int off32 = (int)(((m.block_base % 32) + 32) % 32);
+    const int64_t ng = cdiv(nb + off32, 32);
+    int *gsum = nullptr;
+    SPC5_TRY(dev_alloc(&gsum, (size_t)ng));
+    granule_sums_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng, 8), 148 * 64), 256, 0, st>>>(
+        nb, m.r, m.vs, m.masks, off32, ng, gsum);
+    SPC5_CUDA(cudaGetLastError());
+    unsigned long long *stats = nullptr;
+    SPC5_TRY(dev_alloc(&stats, 2));
+    constexpr int kSlotTarget = 6 * 1024;
+    int chosen = 1;
+    unsigned long long h[2] = {0, 0};
+    for (int k = 32; k >= 1; k >>= 1) {
+        SPC5_CUDA(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st));
+        const int64_t ns = cdiv(ng, k);
+        stage_stats_kernel<<<(unsigned)cdiv(ns, 256), 256, 0, st>>>(ng, k, gsum, nb, off32,
+                                                                     m.rowptr, np, stats,
+                                                                     stats + 1);
+        SPC5_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        const int64_t sb = 32LL * k;
+        const int64_t rp_cap = std::min<int64_t>((int64_t)h[1], sb + 8);
+        const int bytes = slot_bytes_for(sb, (int64_t)h[0], rp_cap, m.r, m.mask_bytes(),
+                                         m.value_bytes());
+        chosen = k;
+        P.stage_vmax = (int64_t)h[0];
+        P.rp_cap = (int)rp_cap;
+        P.slot_bytes = bytes;
+        if (bytes <= kSlotTarget) break;
+    }
+    P.stage_granules = chosen;
+    const int64_t ns = cdiv(ng, chosen);
+    P.num_stages = ns;
+    int64_t *ssum = nullptr;
+    SPC5_TRY(dev_alloc(&ssum, (size_t)ns));
+    SPC5_TRY(dev_alloc(&P.stage_v, (size_t)ns + 1));
+    SPC5_TRY(dev_alloc(&P.stage_p, (size_t)ns + 1));
+    stage_fill_kernel<<<(unsigned)cdiv(ns + 1, 256), 256, 0, st>>>(ng, chosen, gsum, nb, off32,
+                                                                    m.rowptr, np, ns, ssum,
+                                                                    P.stage_p);
+    SPC5_CUDA(cudaGetLastError());
+    SPC5_CUDA(cudaMemsetAsync(P.stage_v, 0, sizeof(int64_t), st));
+    SPC5_TRY(scan_inclusive_i64(ssum, P.stage_v + 1, ns, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    dev_free(ssum);
+    dev_free(gsum);
+    dev_free(stats);
     return SPC5_OK;
 }
 
@@ -401,8 +529,11 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     dev_free(split_incl);
     const int64_t nc = P.num_chunks;
     SPC5_CUDA(cudaMemcpyAsync(P.chunk_b + nc, &nb, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    SPC5_TRY(dev_alloc(&P.chunk_v, (size_t)nc));
-    SPC5_TRY(dev_alloc(&P.chunk_p, (size_t)nc));
+    SPC5_TRY(dev_alloc(&P.chunk_v, (size_t)nc + 1));
+    SPC5_TRY(dev_alloc(&P.chunk_p, (size_t)nc + 1));
+    SPC5_CUDA(cudaMemcpyAsync(P.chunk_v + nc, &m.nnz, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    SPC5_CUDA(cudaMemcpyAsync(P.chunk_p + nc, &m.num_panels, sizeof(int64_t),
+                              cudaMemcpyHostToDevice, st));
     uint8_t *split_flag = nullptr;
     SPC5_TRY(dev_alloc(&split_flag, (size_t)nc));
     chunk_desc_kernel<<<(unsigned)std::min<int64_t>(cdiv(nc, 8), 148 * 32), 256, 0, st>>>(
@@ -417,6 +548,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     SPC5_CUDA(cudaMemcpyAsync(P.h_chunk_b, P.chunk_b, sizeof(int64_t) * (nc + 1),
                               cudaMemcpyDeviceToHost, st));
     SPC5_CUDA(cudaStreamSynchronize(st));
+    SPC5_TRY(build_stages(m, st));
     P.built = true;
     return SPC5_OK;
 }
