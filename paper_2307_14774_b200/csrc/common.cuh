@@ -18,7 +18,6 @@
 namespace spc5 {
 
 constexpr int kTile = 1024;       // blocks per popcount-prefix tile
-constexpr int64_t kSplit = 2048;  // giant panels are cut at global multiples of this
 constexpr int kWarpsPerCta = 8;   // SpMV CTA = 8 warps, one chunk per warp
 
 struct Plan {
@@ -35,15 +34,17 @@ struct Plan {
     int64_t *empty_panels = nullptr;  // [num_empty] panels with no block
     int64_t num_tiles = 0;
     int64_t *tile_prefix = nullptr;   // [num_tiles+1] value offset at tile starts
-    // TMA stages: groups of `stage_granules` 32-block granules aligned to global
-    // multiples of 32 blocks (so no warp window straddles two stages)
-    int stage_granules = 1;
-    int64_t num_stages = 0;
-    int64_t *stage_v = nullptr;  // [num_stages+1] value offset at stage starts (+ nnz)
-    int64_t *stage_p = nullptr;  // [num_stages+1] panel containing the stage start (+ num_panels)
-    int64_t stage_vmax = 0;      // max values in one stage
-    int rp_cap = 0;              // rowptr entries staged per stage (else read from global)
-    int slot_bytes = 0;          // smem bytes of one stage slot
+    // ring slots: one chunk per shared-memory slot
+    int64_t chunk_target = 0;       // blocks per chunk target (snapped to panel starts)
+    int64_t split_len = 256;        // long panels are cut at global multiples of this
+    int64_t max_chunk_blocks = 0, max_chunk_values = 0;
+    int64_t lay_col = 0, lay_mask = 0, lay_val = 0;  // slot layout: bits | col | mask | val
+    int slot_bytes = 0;
+    int64_t num_granules = 0;
+    uint32_t *pstart_bits = nullptr;  // [num_granules] bit i of word g: block 32g-off32+i starts a panel
+    uint8_t *chunk_flags = nullptr;   // [num_chunks] bit0: starts inside a panel, bit1: has empty panels
+    int64_t num_generic = 0;
+    int *generic_chunks = nullptr;    // [num_generic] chunks with flags != 0 (generic pass)
 };
 
 struct Matrix {

@@ -127,7 +127,8 @@ __global__ void targets_kernel(int64_t num_panels, const int64_t *__restrict__ r
 }
 
 // (b) forced splits inside giant panels at global multiples of kSplit
-__device__ __forceinline__ int64_t split_count(int64_t s, int64_t e, int64_t base) {
+__device__ __forceinline__ int64_t split_count(int64_t s, int64_t e, int64_t base,
+                                               int64_t kSplit) {
     if (e - s <= kSplit) return 0;
     const int64_t gs = s + base, ge = e + base;
     // multiples g of kSplit with gs < g < ge
@@ -136,18 +137,19 @@ __device__ __forceinline__ int64_t split_count(int64_t s, int64_t e, int64_t bas
 }
 
 __global__ void split_count_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
-                                   int64_t base, int64_t *counts) {
+                                   int64_t base, int64_t kSplit, int64_t *counts) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= num_panels) return;
-    counts[p] = split_count(rowptr[p], rowptr[p + 1], base);
+    counts[p] = split_count(rowptr[p], rowptr[p + 1], base, kSplit);
 }
 
 __global__ void split_fill_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
-                                  int64_t base, const int64_t *__restrict__ incl, int64_t *out) {
+                                  int64_t base, int64_t kSplit, const int64_t *__restrict__ incl,
+                                  int64_t *out) {
     const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (p >= num_panels) return;
     const int64_t s = rowptr[p], e = rowptr[p + 1];
-    const int64_t n = split_count(s, e, base);
+    const int64_t n = split_count(s, e, base, kSplit);
     if (!n) return;
     int64_t pos = incl[p] - n;
     const int64_t first = (s + base) / kSplit + 1;
@@ -180,65 +182,69 @@ __global__ void empty_flag_kernel(int64_t num_panels, const int64_t *__restrict_
     if (p < num_panels) flag[p] = rowptr[p] == rowptr[p + 1] ? 1 : 0;
 }
 
-// ---- TMA stage plan ---------------------------------------------------------
-// Granule g covers local blocks [gstart(g), gstart(g+1)) with
-// gstart(g) = max(0, 32*g - off32), off32 = block_base mod 32: granule
-// boundaries are global multiples of 32 blocks.
-__device__ __forceinline__ int64_t granule_start(int64_t g, int64_t ng, int64_t nb, int off32) {
-    if (g <= 0) return 0;
-    if (g >= ng) return nb;
-    const int64_t b = g * 32 - off32;
-    return b < nb ? b : nb;
-}
-
-__global__ void granule_sums_kernel(int64_t nb, int r, int vs, const void *__restrict__ masks,
-                                    int off32, int64_t ng, int *gsum) {
-    const int lane = threadIdx.x & 31;
-    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
-    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
-    for (int64_t g = warp; g < ng; g += nwarps) {
-        const int64_t lo = granule_start(g, ng, nb, off32), hi = granule_start(g + 1, ng, nb, off32);
+// ---- ring-slot sizing ------------------------------------------------------
+// largest popcount of one block (all r rows)
+__global__ void max_block_popc_kernel(int64_t nb, int r, int vs, const void *__restrict__ masks,
+                                      unsigned long long *out) {
+    int best = 0;
+    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
+         b += (int64_t)gridDim.x * blockDim.x) {
         int s = 0;
-        const int64_t b = lo + lane;
-        if (b < hi)
-            for (int rr = 0; rr < r; ++rr) s += __popc(load_mask(masks, b * r + rr, vs));
-        s = __reduce_add_sync(0xffffffffu, s);
-        if (lane == 0) gsum[g] = s;
+        for (int rr = 0; rr < r; ++rr) s += __popc(load_mask(masks, b * r + rr, vs));
+        best = max(best, s);
     }
+    best = __reduce_max_sync(0xffffffffu, best);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)best);
 }
 
-// per candidate stage size k (granules): max values and max staged rowptr entries
-__global__ void stage_stats_kernel(int64_t ng, int k, const int *__restrict__ gsum, int64_t nb,
-                                   int off32, const int64_t *__restrict__ rowptr, int64_t np,
-                                   unsigned long long *vmax, unsigned long long *pmax) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    const int64_t ns = cdiv_dev(ng, k);
-    if (j >= ns) return;
-    long long s = 0;
-    for (int64_t g = j * k; g < min((j + 1) * k, ng); ++g) s += gsum[g];
-    atomicMax(vmax, (unsigned long long)s);
-    const int64_t b0 = granule_start(j * k, ng, nb, off32);
-    const int64_t b1 = granule_start((j + 1) * k, ng, nb, off32);
-    const int64_t p0 = upper_bound_dev(rowptr, np, b0) - 1;
-    const int64_t p1 = b1 < nb ? upper_bound_dev(rowptr, np, b1) - 1 : np;
-    const int64_t cnt = min(p1 + 1, np) - p0 + 1;
-    atomicMax(pmax, (unsigned long long)cnt);
+// max blocks and max values of one chunk (a chunk is one shared-memory slot)
+__global__ void chunk_stats_kernel(int64_t nc, const int64_t *__restrict__ chunk_b,
+                                   const int64_t *__restrict__ chunk_v,
+                                   unsigned long long *out /* [2] */) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    atomicMax(out, (unsigned long long)(chunk_b[c + 1] - chunk_b[c]));
+    atomicMax(out + 1, (unsigned long long)(chunk_v[c + 1] - chunk_v[c]));
 }
 
-__global__ void stage_fill_kernel(int64_t ng, int k, const int *__restrict__ gsum, int64_t nb,
-                                  int off32, const int64_t *__restrict__ rowptr, int64_t np,
-                                  int64_t ns, int64_t *stage_sum, int64_t *stage_p) {
-    const int64_t j = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (j > ns) return;
-    if (j == ns) {
-        stage_p[j] = np;
-        return;
+// panel-start bitmap over granules (derived plan data, 1 bit per block)
+__global__ void pstart_bits_kernel(int64_t np, const int64_t *__restrict__ rowptr, int off32,
+                                   uint32_t *bits) {
+    const int64_t p = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (p >= np) return;
+    const int64_t b = rowptr[p];
+    if (b == rowptr[p + 1]) return;  // empty panel: no block starts it
+    atomicOr(bits + ((b + off32) >> 5), 1u << ((b + off32) & 31));
+}
+
+// per chunk: bit0 = first block is not a panel start, bit1 = empty panels inside
+__global__ void chunk_flags_kernel(int64_t nc, const int64_t *__restrict__ chunk_b,
+                                   const int64_t *__restrict__ chunk_p,
+                                   const int64_t *__restrict__ rowptr,
+                                   const int64_t *__restrict__ empty, int64_t ne, uint8_t *flags) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    uint8_t f = rowptr[chunk_p[c]] < chunk_b[c] ? 1 : 0;
+    // any empty panel p with chunk_p[c] < p < chunk_p[c+1]?
+    const int64_t lo_p = chunk_p[c], hi_p = chunk_p[c + 1];
+    int64_t lo = 0, hi = ne;  // first empty panel > lo_p
+    while (lo < hi) {
+        const int64_t mid = (lo + hi) / 2;
+        if (empty[mid] <= lo_p) lo = mid + 1;
+        else hi = mid;
     }
-    long long s = 0;
-    for (int64_t g = j * k; g < min((j + 1) * k, ng); ++g) s += gsum[g];
-    stage_sum[j] = s;
-    const int64_t b0 = granule_start(j * k, ng, nb, off32);
-    stage_p[j] = upper_bound_dev(rowptr, np, b0) - 1;
+    if (lo < ne && empty[lo] < hi_p) f |= 2;
+    flags[c] = f;
+}
+
+__global__ void generic_flag_kernel(int64_t nc, const uint8_t *flags, uint8_t *out) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < nc) out[c] = (flags[c] & 2) ? 1 : 0;  // empty panels inside: generic pass
+}
+
+__global__ void narrow_kernel(const int64_t *in, int64_t n, int *out) {
+    const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (i < n) out[i] = (int)in[i];
 }
 
 // ---- partition_by_nnz ----------------------------------------------------
@@ -335,8 +341,9 @@ void free_plan(Plan &p) {
     dev_free(p.carry);
     dev_free(p.empty_panels);
     dev_free(p.tile_prefix);
-    dev_free(p.stage_v);
-    dev_free(p.stage_p);
+    dev_free(p.pstart_bits);
+    dev_free(p.chunk_flags);
+    dev_free(p.generic_chunks);
     delete[] p.h_chunk_b;
     p = Plan{};
 }
@@ -362,67 +369,100 @@ int validate_structure(const Matrix &m, cudaStream_t st) {
     return SPC5_OK;
 }
 
-// Stage size: the largest power-of-two number of granules whose worst stage
-// (values + headers + staged rowptr) fits kSlotTarget bytes of shared memory.
-static int slot_bytes_for(int64_t sb, int64_t vmax, int64_t rp_cap, int r, int mb, int vb) {
-    auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
-    // +32 per region: a bulk copy is widened to 16-byte alignment at both ends
-    const int64_t bytes = a16(sb * 4 + 32) + a16(sb * r * mb + 32) + a16(rp_cap * 8 + 32) +
-                          a16(vmax * vb + 32);
-    return (int)((bytes + 127) / 128 * 128);
-}
-
-int build_stages(Matrix &m, cudaStream_t st) {
+// Chunk boundaries: a target every `cb` blocks snapped back to the start of
+// the panel holding it, plus -- inside panels longer than kSplit blocks -- the
+// GLOBAL multiples of kSplit (so a long panel is cut where its own position
+// says, independent of cb, shards and ranges).  Fills chunk_b/v/p (+sentinels),
+// the split-chunk list and the carry slots.
+static int build_chunks(Matrix &m, int64_t cb, cudaStream_t st) {
     Plan &P = m.plan;
     const int64_t nb = m.num_blocks, np = m.num_panels;
-    const int off32 = (int)(((m.block_base % 32) + 32) % 32);
-    const int64_t ng = cdiv(nb + off32, 32);
-    int *gsum = nullptr;
-    SPC5_TRY(dev_alloc(&gsum, (size_t)ng));
-    granule_sums_kernel<<<(unsigned)std::min<int64_t>(cdiv(ng, 8), 148 * 64), 256, 0, st>>>(
-        nb, m.r, m.vs, m.masks, off32, ng, gsum);
-    SPC5_CUDA(cudaGetLastError());
-    unsigned long long *stats = nullptr;
-    SPC5_TRY(dev_alloc(&stats, 2));
-    constexpr int kSlotTarget = 6 * 1024;
-    int chosen = 1;
-    unsigned long long h[2] = {0, 0};
-    for (int k = 32; k >= 1; k >>= 1) {
-        SPC5_CUDA(cudaMemsetAsync(stats, 0, 2 * sizeof(unsigned long long), st));
-        const int64_t ns = cdiv(ng, k);
-        stage_stats_kernel<<<(unsigned)cdiv(ns, 256), 256, 0, st>>>(ng, k, gsum, nb, off32,
-                                                                     m.rowptr, np, stats,
-                                                                     stats + 1);
-        SPC5_CUDA(cudaMemcpyAsync(h, stats, sizeof(h), cudaMemcpyDeviceToHost, st));
-        SPC5_CUDA(cudaStreamSynchronize(st));
-        const int64_t sb = 32LL * k;
-        const int64_t rp_cap = std::min<int64_t>((int64_t)h[1], sb + 8);
-        const int bytes = slot_bytes_for(sb, (int64_t)h[0], rp_cap, m.r, m.mask_bytes(),
-                                         m.value_bytes());
-        chosen = k;
-        P.stage_vmax = (int64_t)h[0];
-        P.rp_cap = (int)rp_cap;
-        P.slot_bytes = bytes;
-        if (bytes <= kSlotTarget) break;
-    }
-    P.stage_granules = chosen;
-    const int64_t ns = cdiv(ng, chosen);
-    P.num_stages = ns;
-    int64_t *ssum = nullptr;
-    SPC5_TRY(dev_alloc(&ssum, (size_t)ns));
-    SPC5_TRY(dev_alloc(&P.stage_v, (size_t)ns + 1));
-    SPC5_TRY(dev_alloc(&P.stage_p, (size_t)ns + 1));
-    stage_fill_kernel<<<(unsigned)cdiv(ns + 1, 256), 256, 0, st>>>(ng, chosen, gsum, nb, off32,
-                                                                    m.rowptr, np, ns, ssum,
-                                                                    P.stage_p);
-    SPC5_CUDA(cudaGetLastError());
-    SPC5_CUDA(cudaMemsetAsync(P.stage_v, 0, sizeof(int64_t), st));
-    SPC5_TRY(scan_inclusive_i64(ssum, P.stage_v + 1, ns, st));
+    const int64_t num_targets = cdiv(nb, cb);
+    int64_t *split_counts = nullptr;
+    SPC5_TRY(dev_alloc(&split_counts, (size_t)np));
+    split_count_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
+                                                                 P.split_len, split_counts);
+    int64_t *split_incl = nullptr;
+    SPC5_TRY(dev_alloc(&split_incl, (size_t)np));
+    SPC5_TRY(scan_inclusive_i64(split_counts, split_incl, np, st));
+    int64_t num_forced = 0;
+    SPC5_CUDA(cudaMemcpyAsync(&num_forced, split_incl + np - 1, sizeof(int64_t),
+                              cudaMemcpyDeviceToHost, st));
     SPC5_CUDA(cudaStreamSynchronize(st));
-    dev_free(ssum);
-    dev_free(gsum);
-    dev_free(stats);
+    const int64_t ncand = num_targets + num_forced;
+    int64_t *cand = nullptr, *sorted = nullptr;
+    SPC5_TRY(dev_alloc(&cand, (size_t)ncand));
+    SPC5_TRY(dev_alloc(&sorted, (size_t)ncand + 1));
+    targets_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(np, m.rowptr, cb,
+                                                                      num_targets, cand);
+    if (num_forced)
+        split_fill_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
+                                                                    P.split_len, split_incl,
+                                                                    cand + num_targets);
+    SPC5_CUDA(cudaGetLastError());
+    {
+        size_t bytes = 0;
+        SPC5_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, cand, sorted, ncand, 0, 64, st));
+        void *tmp = nullptr;
+        SPC5_TRY(dev_alloc(&tmp, bytes));
+        SPC5_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, cand, sorted, ncand, 0, 64, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(tmp);
+    }
+    int64_t *d_nuniq = nullptr;
+    SPC5_TRY(dev_alloc(&d_nuniq, 1));
+    SPC5_TRY(dev_alloc(&P.chunk_b, (size_t)ncand + 1));
+    {
+        size_t bytes = 0;
+        SPC5_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, sorted, P.chunk_b, d_nuniq, ncand, st));
+        void *tmp = nullptr;
+        SPC5_TRY(dev_alloc(&tmp, bytes));
+        SPC5_CUDA(cub::DeviceSelect::Unique(tmp, bytes, sorted, P.chunk_b, d_nuniq, ncand, st));
+        SPC5_CUDA(cudaMemcpyAsync(&P.num_chunks, d_nuniq, sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                  st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(tmp);
+    }
+    dev_free(d_nuniq);
+    dev_free(cand);
+    dev_free(sorted);
+    dev_free(split_counts);
+    dev_free(split_incl);
+    const int64_t nc = P.num_chunks;
+    SPC5_CUDA(cudaMemcpyAsync(P.chunk_b + nc, &nb, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    SPC5_TRY(dev_alloc(&P.chunk_v, (size_t)nc + 1));
+    SPC5_TRY(dev_alloc(&P.chunk_p, (size_t)nc + 1));
+    SPC5_CUDA(cudaMemcpyAsync(P.chunk_v + nc, &m.nnz, sizeof(int64_t), cudaMemcpyHostToDevice, st));
+    SPC5_CUDA(cudaMemcpyAsync(P.chunk_p + nc, &m.num_panels, sizeof(int64_t),
+                              cudaMemcpyHostToDevice, st));
+    uint8_t *split_flag = nullptr;
+    SPC5_TRY(dev_alloc(&split_flag, (size_t)nc));
+    chunk_desc_kernel<<<(unsigned)std::min<int64_t>(cdiv(nc, 8), 148 * 32), 256, 0, st>>>(
+        nc, np, m.r, m.vs, m.rowptr, m.masks, P.tile_prefix, P.chunk_b, P.chunk_v, P.chunk_p,
+        split_flag);
+    SPC5_CUDA(cudaGetLastError());
+    SPC5_TRY(dev_alloc(&P.split_chunks, (size_t)nc));
+    SPC5_TRY(select_flagged(split_flag, nc, P.split_chunks, &P.num_split, st));
+    dev_free(split_flag);
+    if (P.num_split) SPC5_TRY(dev_alloc(&P.carry, (size_t)nc * m.r));
+    P.h_chunk_b = new int64_t[nc + 1];
+    SPC5_CUDA(cudaMemcpyAsync(P.h_chunk_b, P.chunk_b, sizeof(int64_t) * (nc + 1),
+                              cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
     return SPC5_OK;
+}
+
+static void free_chunks(Plan &P) {
+    dev_free(P.chunk_b);
+    dev_free(P.chunk_v);
+    dev_free(P.chunk_p);
+    dev_free(P.split_chunks);
+    dev_free(P.carry);
+    delete[] P.h_chunk_b;
+    P.chunk_b = P.chunk_v = P.chunk_p = P.split_chunks = nullptr;
+    P.carry = nullptr;
+    P.h_chunk_b = nullptr;
+    P.num_chunks = P.num_split = 0;
 }
 
 int build_plan(Matrix &m, bool validate, cudaStream_t st) {
@@ -473,82 +513,80 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.built = true;
         return SPC5_OK;
     }
-    // chunk granularity: ~4 chunks per resident warp, multiple of 32, [32, 1024]
-    const int64_t resident_warps = (int64_t)m.sm_count * 32;
-    int64_t cb = cdiv(nb, resident_warps * 4);
-    cb = std::max<int64_t>(32, std::min<int64_t>(1024, cdiv(cb, 32) * 32));
-    const int64_t num_targets = cdiv(nb, cb);
-    int64_t *split_counts = nullptr;
-    SPC5_TRY(dev_alloc(&split_counts, (size_t)np));
-    split_count_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
-                                                                 split_counts);
-    int64_t *split_incl = nullptr;
-    SPC5_TRY(dev_alloc(&split_incl, (size_t)np));
-    SPC5_TRY(scan_inclusive_i64(split_counts, split_incl, np, st));
-    int64_t num_forced = 0;
-    SPC5_CUDA(cudaMemcpyAsync(&num_forced, split_incl + np - 1, sizeof(int64_t),
-                              cudaMemcpyDeviceToHost, st));
-    SPC5_CUDA(cudaStreamSynchronize(st));
-    const int64_t ncand = num_targets + num_forced;
-    int64_t *cand = nullptr, *sorted = nullptr;
-    SPC5_TRY(dev_alloc(&cand, (size_t)ncand));
-    SPC5_TRY(dev_alloc(&sorted, (size_t)ncand + 1));
-    targets_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(np, m.rowptr, cb,
-                                                                      num_targets, cand);
-    if (num_forced)
-        split_fill_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
-                                                                    split_incl,
-                                                                    cand + num_targets);
+    // Long panels are cut every split_len blocks (at global multiples) with
+    // split_len sized so a piece fits one slot; chunks = ring slots, the
+    // largest target size whose worst chunk fits the slot target.
+    {
+        unsigned long long *d_mx = nullptr, h_mx = 0;
+        SPC5_TRY(dev_alloc(&d_mx, 1));
+        SPC5_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
+        max_block_popc_kernel<<<(unsigned)std::min<int64_t>(cdiv(nb, 256), 148 * 16), 256, 0,
+                                st>>>(nb, m.r, m.vs, m.masks, d_mx);
+        SPC5_CUDA(cudaMemcpyAsync(&h_mx, d_mx, sizeof(h_mx), cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(d_mx);
+        const int64_t max_block_bytes = 4 + m.r * m.mask_bytes() + (int64_t)h_mx * m.value_bytes();
+        int64_t sl = 256;
+        while (sl > 1 && sl * max_block_bytes > 6 * 1024) sl >>= 1;
+        P.split_len = sl;
+    }
+    for (int64_t cb = 256;; cb >>= 1) {
+        SPC5_TRY(build_chunks(m, cb, st));
+        unsigned long long *d_st = nullptr, h_st[2] = {0, 0};
+        SPC5_TRY(dev_alloc(&d_st, 2));
+        SPC5_CUDA(cudaMemsetAsync(d_st, 0, 2 * sizeof(unsigned long long), st));
+        chunk_stats_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
+            P.num_chunks, P.chunk_b, P.chunk_v, d_st);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(d_st);
+        P.max_chunk_blocks = (int64_t)h_st[0];
+        P.max_chunk_values = (int64_t)h_st[1];
+        P.chunk_target = cb;
+        auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
+        const int64_t mb = P.max_chunk_blocks;
+        P.lay_col = a16((mb / 32 + 2) * 4 + 32);
+        P.lay_mask = P.lay_col + a16(mb * 4 + 32);
+        P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);
+        P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
+                             128 * 128);
+        if (P.slot_bytes <= 6 * 1024 || cb == 1) break;
+        if (cb <= 32 && P.slot_bytes <= 14 * 1024) break;
+        free_chunks(P);
+    }
+    if (P.slot_bytes > 14 * 1024)
+        return fail(SPC5_EINVAL, "a chunk of this matrix does not fit the shared-memory ring");
+    // panel-start bitmap, chunk flags, the generic pass's chunk list
+    const int off32 = (int)(((m.block_base % 32) + 32) % 32);
+    const int64_t ng = cdiv(nb + off32, 32);
+    P.num_granules = ng;
+    SPC5_TRY(dev_alloc(&P.pstart_bits, (size_t)ng + 4));
+    SPC5_CUDA(cudaMemsetAsync(P.pstart_bits, 0, sizeof(uint32_t) * (ng + 4), st));
+    pstart_bits_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, off32,
+                                                                 P.pstart_bits);
+    SPC5_CUDA(cudaGetLastError());
+    SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
+    chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
+        P.num_chunks, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels, P.num_empty,
+        P.chunk_flags);
     SPC5_CUDA(cudaGetLastError());
     {
-        size_t bytes = 0;
-        SPC5_CUDA(cub::DeviceRadixSort::SortKeys(nullptr, bytes, cand, sorted, ncand, 0, 64, st));
-        void *tmp = nullptr;
-        SPC5_TRY(dev_alloc(&tmp, bytes));
-        SPC5_CUDA(cub::DeviceRadixSort::SortKeys(tmp, bytes, cand, sorted, ncand, 0, 64, st));
+        int64_t *list64 = nullptr;
+        uint8_t *gflag = nullptr;
+        SPC5_TRY(dev_alloc(&list64, (size_t)P.num_chunks));
+        SPC5_TRY(dev_alloc(&gflag, (size_t)P.num_chunks));
+        generic_flag_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
+            P.num_chunks, P.chunk_flags, gflag);
+        SPC5_TRY(select_flagged(gflag, P.num_chunks, list64, &P.num_generic, st));
+        SPC5_TRY(dev_alloc(&P.generic_chunks, (size_t)std::max<int64_t>(P.num_generic, 1)));
+        if (P.num_generic)
+            narrow_kernel<<<(unsigned)cdiv(P.num_generic, 256), 256, 0, st>>>(
+                list64, P.num_generic, P.generic_chunks);
         SPC5_CUDA(cudaStreamSynchronize(st));
-        dev_free(tmp);
+        dev_free(list64);
+        dev_free(gflag);
     }
-    int64_t *d_nuniq = nullptr;
-    SPC5_TRY(dev_alloc(&d_nuniq, 1));
-    SPC5_TRY(dev_alloc(&P.chunk_b, (size_t)ncand + 1));
-    {
-        size_t bytes = 0;
-        SPC5_CUDA(cub::DeviceSelect::Unique(nullptr, bytes, sorted, P.chunk_b, d_nuniq, ncand, st));
-        void *tmp = nullptr;
-        SPC5_TRY(dev_alloc(&tmp, bytes));
-        SPC5_CUDA(cub::DeviceSelect::Unique(tmp, bytes, sorted, P.chunk_b, d_nuniq, ncand, st));
-        SPC5_CUDA(cudaMemcpyAsync(&P.num_chunks, d_nuniq, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SPC5_CUDA(cudaStreamSynchronize(st));
-        dev_free(tmp);
-    }
-    dev_free(d_nuniq);
-    dev_free(cand);
-    dev_free(sorted);
-    dev_free(split_counts);
-    dev_free(split_incl);
-    const int64_t nc = P.num_chunks;
-    SPC5_CUDA(cudaMemcpyAsync(P.chunk_b + nc, &nb, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    SPC5_TRY(dev_alloc(&P.chunk_v, (size_t)nc + 1));
-    SPC5_TRY(dev_alloc(&P.chunk_p, (size_t)nc + 1));
-    SPC5_CUDA(cudaMemcpyAsync(P.chunk_v + nc, &m.nnz, sizeof(int64_t), cudaMemcpyHostToDevice, st));
-    SPC5_CUDA(cudaMemcpyAsync(P.chunk_p + nc, &m.num_panels, sizeof(int64_t),
-                              cudaMemcpyHostToDevice, st));
-    uint8_t *split_flag = nullptr;
-    SPC5_TRY(dev_alloc(&split_flag, (size_t)nc));
-    chunk_desc_kernel<<<(unsigned)std::min<int64_t>(cdiv(nc, 8), 148 * 32), 256, 0, st>>>(
-        nc, np, m.r, m.vs, m.rowptr, m.masks, P.tile_prefix, P.chunk_b, P.chunk_v, P.chunk_p,
-        split_flag);
-    SPC5_CUDA(cudaGetLastError());
-    SPC5_TRY(dev_alloc(&P.split_chunks, (size_t)nc));
-    SPC5_TRY(select_flagged(split_flag, nc, P.split_chunks, &P.num_split, st));
-    dev_free(split_flag);
-    if (P.num_split) SPC5_TRY(dev_alloc(&P.carry, (size_t)nc * m.r));
-    P.h_chunk_b = new int64_t[nc + 1];
-    SPC5_CUDA(cudaMemcpyAsync(P.h_chunk_b, P.chunk_b, sizeof(int64_t) * (nc + 1),
-                              cudaMemcpyDeviceToHost, st));
-    SPC5_CUDA(cudaStreamSynchronize(st));
-    SPC5_TRY(build_stages(m, st));
     P.built = true;
     return SPC5_OK;
 }

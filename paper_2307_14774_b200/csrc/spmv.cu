@@ -1,25 +1,31 @@
 // spmv.cu -- K2: y (+)= A.x over the SPC5 beta(r,vs) arrays on sm_100a.
 //
 // Replaces spmv_spc5_scalar / spmv_spc5_vector (kernels.py:121-230), i.e.
-// Algorithm 1 of the paper re-mapped to a warp:
+// Algorithm 1 of the paper re-mapped to a B200 warp:
 //
-//  * lane-per-block: a warp walks its chunk in 32-block windows aligned to
-//    GLOBAL block indices; lane l owns block w+l.  Its column start and its r
-//    masks come in with one coalesced load each (r*mask_bytes <= 16 B).
-//  * value offsets: popcount of the lane's masks + a warp inclusive scan
-//    (5 shuffles) on top of the chunk's offset from the plan -- the
-//    "value cursor" of kernels.py:211-212 in parallel form.
-//  * panel of each block: one coalesced load of the next 32 block_rowptr
-//    entries and a 5-step shuffle binary search (empty panels and >32 panel
-//    ends per window take a global binary search).
-//  * the lane walks its set bits (__ffs), multiplying packed values by x
-//    (read-only path; x is the only re-read array and stays L2 resident) into
-//    r per-row accumulators (fp64; products formed in the matrix precision).
+//  * TMA streaming.  The plan cuts the block array into chunks of ~32-256
+//    blocks (starts snapped to panel starts).  Each warp owns a ring of
+//    kSlots shared-memory slots; one lane fills a slot with a chunk's
+//    panel-start bits, column starts, masks and packed values using four
+//    cp.async.bulk copies completing on one mbarrier (SASS UBLKCP /
+//    SYNCS), so the matrix stream never sits in registers and the next
+//    kSlots-1 chunks are in flight while one is consumed.
+//  * lane-per-block.  The warp walks its chunk in 32-block windows aligned to
+//    GLOBAL block indices; lane l owns block w+l (all R rows of it).
+//  * value offsets: popcount of the lane's masks + a warp inclusive scan --
+//    the "value cursor" of kernels.py:211-212 in parallel form.
+//  * panel membership: one bit per block from the plan's panel-start bitmap
+//    (a popcount gives the panel of every lane); chunks holding empty panels
+//    search block_rowptr instead (generic pass).
+//  * products: each panel row's set bits, highest first (bfind), x gathered
+//    through the read-only path (x is the only re-read array and stays L2
+//    resident; the matrix stream is loaded evict-first), fp64 accumulation
+//    of products formed in the matrix precision.
 //  * per-row reduction: a segmented warp scan over lanes of the same panel;
-//    the segment tail writes y (or carries into the next window).  Chunks
-//    that start inside a giant panel write their head segment to a carry slot
-//    and a tiny fixup kernel adds those in chunk order.  Every panel is summed
-//    in an order fixed by global block positions only, so results are
+//    segment tails store y; the last segment of a window is carried into the
+//    next one.  Chunks starting inside a long panel write their head segment
+//    to a carry slot that a fixup kernel adds in chunk order.  Every panel is
+//    summed in an order fixed by global block positions only, so results are
 //    bitwise reproducible across runs, spmv_parallel ranges and GPU shards.
 #include <algorithm>
 
@@ -37,35 +43,23 @@ struct SpmvArgs {
     void *y;
     int64_t num_rows, num_panels;
     const int64_t *chunk_b, *chunk_v, *chunk_p;
-    int64_t c_lo, c_hi;  // chunk range
-    int64_t b_lo, b_hi;  // compute-active block range
-    int64_t p_lo, p_hi;  // panels whose rows may be written
+    const uint8_t *chunk_flags;   // bit0 starts inside a panel, bit1 has empty panels
+    const uint32_t *pstart_bits;  // panel-start bitmap over 32-block granules
+    const int *chunk_list;        // generic pass over a list of chunks (else null)
+    int64_t c_lo, c_hi;           // chunk index range (into chunk_list when set)
+    int64_t b_lo, b_hi;           // blocks contributing to y
+    int64_t p_lo, p_hi;           // panels whose rows may be written
     double *carry;
     const int64_t *empty_panels;
     int64_t num_empty;
-    int base_mod;  // block_base mod 32
+    int off32;         // block_base mod 32 (window alignment)
     int accumulate;
-    // TMA stage plan
-    const int64_t *stage_v, *stage_p;
-    int stage_k;  // 32-block granules per stage
-    int off32;    // block_base mod 32 (granule alignment)
-    int rp_cap;   // staged rowptr entries per stage
-    uint32_t lay_mask, lay_rp, lay_val, lay_bytes;  // slot layout (bytes)
+    int skip_generic;  // fast pass: leave chunks with empty panels to the generic pass
+    uint32_t lay_col, lay_mask, lay_val, lay_bytes;  // slot layout (bytes)
 };
 
-
-template <typename T>
-__device__ __forceinline__ double mul_acc(double acc, T v, T xv);
-template <>
-__device__ __forceinline__ double mul_acc<double>(double acc, double v, double xv) {
-    return fma(v, xv, acc);
-}
-template <>
-__device__ __forceinline__ double mul_acc<float>(double acc, float v, float xv) {
-    return acc + (double)(v * xv);  // product rounded in f32, as the reference forms it
-}
-
 constexpr unsigned kFull = 0xffffffffu;
+constexpr int kSlots = 2;  // chunks in flight per warp
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -92,11 +86,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t parity) {
         : "memory");
 }
 // 1-D bulk copy global -> shared, completion counted on `bar` (SASS: UBLKCP)
-__device__ __forceinline__ void bulk_g2s(void *dst, const void *src, uint32_t bytes,
+__device__ __forceinline__ void bulk_g2s(uint32_t dst, const void *src, uint32_t bytes,
                                          uint64_t *bar, uint64_t policy) {
     asm volatile(
         "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes.L2::cache_hint "
-        "[%0], [%1], %2, [%3], %4;" ::"r"(smem_addr(dst)),
+        "[%0], [%1], %2, [%3], %4;" ::"r"(dst),
         "l"(src), "r"(bytes), "r"(smem_addr(bar)), "l"(policy)
         : "memory");
 }
@@ -106,80 +100,201 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
     return pol;
 }
 
-// Exclusive prefix sum over the warp of a small count (< 2^NP) via bit-plane
-// ballots: independent BALLOT/POPC pairs instead of a dependent shuffle chain.
-template <int NP>
-__device__ __forceinline__ void warp_prefix(int cnt, int lane, int &excl, int &total) {
-    const unsigned lt = (1u << lane) - 1u;
-    excl = 0;
-    total = 0;
+__device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    uint32_t v;
+    asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// A lane's R masks (R * sizeof(MT) <= 16 bytes) from shared memory.
+template <int BYTES>
+struct LaneMasks {
+    static constexpr int N = (BYTES + 3) / 4;
+    uint32_t w[N];
+    __device__ __forceinline__ void load(uint32_t addr) {
+        if constexpr (BYTES == 1) {
+            asm volatile("ld.shared.u8 %0, [%1];" : "=r"(w[0]) : "r"(addr));
+        } else if constexpr (BYTES == 2) {
+            asm volatile("ld.shared.u16 %0, [%1];" : "=r"(w[0]) : "r"(addr));
+        } else if constexpr (BYTES == 4) {
+            asm volatile("ld.shared.u32 %0, [%1];" : "=r"(w[0]) : "r"(addr));
+        } else if constexpr (BYTES == 8) {
+            asm volatile("ld.shared.v2.u32 {%0, %1}, [%2];" : "=r"(w[0]), "=r"(w[1]) : "r"(addr));
+        } else {
+            asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                         : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3])
+                         : "r"(addr));
+        }
+    }
+    __device__ __forceinline__ void clear_if(bool keep) {
 #pragma unroll
-    for (int p = 0; p < NP; ++p) {
-        const unsigned bal = __ballot_sync(kFull, (cnt >> p) & 1);
-        excl += __popc(bal & lt) << p;
-        total += __popc(bal) << p;
+        for (int i = 0; i < N; ++i) w[i] = keep ? w[i] : 0u;
+    }
+    __device__ __forceinline__ int popc() const {
+        int c = 0;
+#pragma unroll
+        for (int i = 0; i < N; ++i) c += __popc(w[i]);
+        return c;
+    }
+    template <int MB>
+    __device__ __forceinline__ uint32_t row(int g) const {  // g: compile-time index
+        constexpr uint32_t M = MB == 1 ? 0xffu : 0xffffu;
+        return (w[(g * MB) / 4] >> (((g * MB) % 4) * 8)) & M;
+    }
+};
+
+__device__ __forceinline__ double ldg_pred(const double *p, bool pred) {
+    double v = 0.0;
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f64 %0, [%1];\n}"
+        : "+d"(v)
+        : "l"(p), "r"((int)pred));
+    return v;
+}
+__device__ __forceinline__ float ldg_pred(const float *p, bool pred) {
+    float v = 0.0f;
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f32 %0, [%1];\n}"
+        : "+f"(v)
+        : "l"(p), "r"((int)pred));
+    return v;
+}
+template <typename T>
+__device__ __forceinline__ T lds_pred(uint32_t addr, bool pred);
+template <>
+__device__ __forceinline__ double lds_pred<double>(uint32_t addr, bool pred) {
+    double v = 0.0;
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}"
+                 : "+d"(v)
+                 : "r"(addr), "r"((int)pred));
+    return v;
+}
+template <>
+__device__ __forceinline__ float lds_pred<float>(uint32_t addr, bool pred) {
+    float v = 0.0f;
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f32 %0, [%1];\n}"
+                 : "+f"(v)
+                 : "r"(addr), "r"((int)pred));
+    return v;
+}
+
+// acc += v * x: fused for f64; for f32 the product is rounded in f32 (as the
+// reference forms it) and accumulated in f64.  Empty slots add exact zeros.
+template <typename T>
+__device__ __forceinline__ void mac(double &acc, T v, T xv);
+template <>
+__device__ __forceinline__ void mac<double>(double &acc, double v, double xv) {
+    acc = fma(v, xv, acc);
+}
+template <>
+__device__ __forceinline__ void mac<float>(double &acc, float v, float xv) {
+    acc += (double)__fmul_rn(v, xv);
+}
+
+// highest set bit of a non-zero word (PTX bfind -> SASS FLO)
+__device__ __forceinline__ uint32_t bfind(uint32_t m) {
+    uint32_t r;
+    asm("bfind.u32 %0, %1;" : "=r"(r) : "r"(m));
+    return r;
+}
+
+// warp inclusive scan of small ints (shfl.up with its in-range predicate)
+__device__ __forceinline__ int warp_incl_scan(int v) {
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+        asm("{\n .reg .s32 t;\n .reg .pred p;\n"
+            " shfl.sync.up.b32 t|p, %0, %1, 0, -1;\n"
+            " @p add.s32 %0, %0, t;\n}"
+            : "+r"(v)
+            : "r"(d));
+    }
+    return v;
+}
+
+template <typename T, int G>
+__device__ __forceinline__ void store_rows(T *y, int64_t row0, int64_t num_rows, const double *acc,
+                                           int accumulate) {
+#pragma unroll
+    for (int g = 0; g < G; ++g) {
+        const int64_t row = row0 + g;
+        if (row < num_rows) {
+            const T sv = (T)acc[g];
+            y[row] = accumulate ? y[row] + sv : sv;
+        }
     }
 }
 
-// One stage = the blocks [start, end) of a chunk that fall in one plan stage.
-struct StageDesc {
-    int64_t start, end;  // blocks
-    int64_t v_s, v_e;    // values
-    int64_t p_s, p_e;    // panel holding `start`, panel holding `end` (num_panels at nb)
-};
-
-__device__ __forceinline__ int64_t stage_of(int64_t b, int off32, int k) {
-    return ((b + off32) >> 5) / k;
+// Products of one panel row of one block: up to NS set bits, highest first.
+// Slots past the row's count load nothing and add exact zeros.
+template <typename T, int NS>
+__device__ __forceinline__ void row_slots(double &acc, uint32_t &m, int &hi, const T *xcol,
+                                          uint32_t vaddr) {
+    T vv[NS], xv[NS];
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+        const bool valid = m != 0u;
+        const uint32_t pos = bfind(m);
+        m &= ~(1u << pos);
+        --hi;
+        xv[u] = ldg_pred(xcol + pos, valid);
+        vv[u] = lds_pred<T>(vaddr + (uint32_t)hi * (uint32_t)sizeof(T), valid);
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) mac<T>(acc, vv[u], xv[u]);
 }
 
-__device__ __forceinline__ StageDesc stage_desc(const SpmvArgs &a, int64_t c, int64_t j) {
-    const int64_t cb0 = a.chunk_b[c], cb1 = a.chunk_b[c + 1];
-    const int64_t g0 = j * a.stage_k, g1 = (j + 1) * a.stage_k;
-    const int64_t s0 = g0 == 0 ? 0 : g0 * 32 - a.off32;
-    const int64_t s1 = g1 * 32 - a.off32;
-    StageDesc d;
-    const bool first = s0 <= cb0, lastc = s1 >= cb1;
-    d.start = first ? cb0 : s0;
-    d.end = lastc ? cb1 : s1;
-    d.v_s = first ? a.chunk_v[c] : a.stage_v[j];
-    d.v_e = lastc ? a.chunk_v[c + 1] : a.stage_v[j + 1];
-    d.p_s = first ? a.chunk_p[c] : a.stage_p[j];
-    d.p_e = lastc ? a.chunk_p[c + 1] : a.stage_p[j + 1];
-    return d;
+__device__ __forceinline__ uint64_t align_dn16(uint64_t v) { return v & ~uint64_t(15); }
+__device__ __forceinline__ uint64_t align_up16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
+
+// Lane 0 of the warp: copy chunk c (panel-start words, column starts, masks,
+// values) into the slot at shared address `slot` with four bulk copies that
+// complete on one mbarrier.
+template <typename T, int LB>
+__device__ __forceinline__ void issue_chunk(const SpmvArgs &a, int64_t c, uint32_t slot,
+                                            uint64_t *bar, uint64_t pol) {
+    const int64_t b0 = a.chunk_b[c], b1 = a.chunk_b[c + 1];
+    const int64_t v0 = a.chunk_v[c], v1 = a.chunk_v[c + 1];
+    const uint64_t w0 = (uint64_t)(a.pstart_bits + ((b0 + a.off32) >> 5));
+    const uint64_t w1 = (uint64_t)(a.pstart_bits + ((b1 - 1 + a.off32) >> 5) + 1);
+    const uint64_t c0 = (uint64_t)(a.colidx + b0), c1 = (uint64_t)(a.colidx + b1);
+    const uint64_t m0 = (uint64_t)((const uint8_t *)a.masks + b0 * LB);
+    const uint64_t m1 = (uint64_t)((const uint8_t *)a.masks + b1 * LB);
+    const uint64_t q0 = (uint64_t)((const T *)a.values + v0);
+    const uint64_t q1 = (uint64_t)((const T *)a.values + v1);
+    const uint32_t bw = (uint32_t)(align_up16(w1) - align_dn16(w0));
+    const uint32_t bc = (uint32_t)(align_up16(c1) - align_dn16(c0));
+    const uint32_t bm = (uint32_t)(align_up16(m1) - align_dn16(m0));
+    const uint32_t bv = v1 > v0 ? (uint32_t)(align_up16(q1) - align_dn16(q0)) : 0u;
+    mbar_expect_tx(bar, bw + bc + bm + bv);
+    bulk_g2s(slot, (const void *)align_dn16(w0), bw, bar, pol);
+    bulk_g2s(slot + a.lay_col, (const void *)align_dn16(c0), bc, bar, pol);
+    bulk_g2s(slot + a.lay_mask, (const void *)align_dn16(m0), bm, bar, pol);
+    if (bv) bulk_g2s(slot + a.lay_val, (const void *)align_dn16(q0), bv, bar, pol);
 }
 
-// Warp-uniform cursor over the warp's (chunk, stage) stream.
+// Warp-uniform cursor over the warp's chunks: chunk slots gi*kWarpsPerCta+warp
+// for gi = blockIdx.x, +gridDim.x, ... of [c_lo, c_hi) (or of chunk_list).
 struct Cursor {
-    int64_t gi;  // chunk-group index (blockIdx.x + t * gridDim.x)
-    int64_t c;   // chunk
-    int64_t j, jl;  // current stage, last stage of the chunk
+    int gi;
+    int c;
     bool valid;
 };
 
-__device__ __forceinline__ bool chunk_stages(const SpmvArgs &a, int64_t c, int64_t &j0,
-                                             int64_t &j1) {
-    const int64_t cb0 = a.chunk_b[c], cb1 = a.chunk_b[c + 1];
-    const int64_t b0 = max(cb0, a.b_lo), b1 = min(cb1, a.b_hi);
-    if (b0 >= b1) return false;
-    j0 = stage_of(b0, a.off32, a.stage_k);
-    j1 = stage_of(b1 - 1, a.off32, a.stage_k);
-    return true;
-}
-
+template <bool GENERIC>
 __device__ __forceinline__ void cursor_seek(const SpmvArgs &a, Cursor &cu, int warp) {
-    // first chunk at or after cu.gi that has work
     const int64_t nc = a.c_hi - a.c_lo;
     for (;;) {
-        if (cu.gi * kWarpsPerCta >= nc) {
+        const int64_t s = (int64_t)cu.gi * kWarpsPerCta + warp;
+        if (s >= nc) {
             cu.valid = false;
             return;
         }
-        cu.c = a.c_lo + cu.gi * kWarpsPerCta + warp;
-        if (cu.c >= a.c_hi) {
-            cu.valid = false;
-            return;
+        cu.c = GENERIC && a.chunk_list ? a.chunk_list[a.c_lo + s] : (int)(a.c_lo + s);
+        bool take = true;
+        if (!GENERIC) {
+            take = !a.skip_generic || !(a.chunk_flags[cu.c] & 2);
+        } else if (!a.chunk_list) {  // panel range: chunks overlapping [b_lo, b_hi)
+            take = a.chunk_b[cu.c + 1] > a.b_lo && a.chunk_b[cu.c] < a.b_hi;
         }
-        if (chunk_stages(a, cu.c, cu.j, cu.jl)) {
+        if (take) {
             cu.valid = true;
             return;
         }
@@ -187,86 +302,22 @@ __device__ __forceinline__ void cursor_seek(const SpmvArgs &a, Cursor &cu, int w
     }
 }
 
-__device__ __forceinline__ void cursor_next(const SpmvArgs &a, Cursor &cu, int warp) {
-    if (cu.j < cu.jl) {
-        ++cu.j;
-        return;
-    }
-    cu.gi += gridDim.x;
-    cursor_seek(a, cu, warp);
-}
-
-struct SlotLayout {
-    uint32_t off_mask, off_rp, off_val, bytes;
-};
-
-__device__ __forceinline__ uint64_t align_dn16(uint64_t v) { return v & ~uint64_t(15); }
-__device__ __forceinline__ uint64_t align_up16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
-
-// Lane 0 of the warp: copy one stage's four regions into a slot.
-template <typename T, typename MT, int R>
-__device__ __forceinline__ void issue_stage(const SpmvArgs &a, const StageDesc &d, uint8_t *slot,
-                                            const SlotLayout &lay, uint64_t *bar, uint64_t pol) {
-    constexpr int MB = (int)sizeof(MT);
-    const uint64_t c0 = (uint64_t)(a.colidx + d.start), c1 = (uint64_t)(a.colidx + d.end);
-    const uint64_t m0 = (uint64_t)((const uint8_t *)a.masks + d.start * R * MB);
-    const uint64_t m1 = (uint64_t)((const uint8_t *)a.masks + d.end * R * MB);
-    const int64_t rp_last = min(d.p_e + 1, a.num_panels);
-    const bool rp_staged = rp_last - d.p_s + 1 <= a.rp_cap;
-    const uint64_t r0 = (uint64_t)(a.rowptr + d.p_s), r1 = (uint64_t)(a.rowptr + rp_last + 1);
-    const uint64_t v0 = (uint64_t)((const T *)a.values + d.v_s);
-    const uint64_t v1 = (uint64_t)((const T *)a.values + d.v_e);
-    const uint32_t bc = (uint32_t)(align_up16(c1) - align_dn16(c0));
-    const uint32_t bm = (uint32_t)(align_up16(m1) - align_dn16(m0));
-    const uint32_t br = rp_staged ? (uint32_t)(align_up16(r1) - align_dn16(r0)) : 0u;
-    const uint32_t bv = d.v_e > d.v_s ? (uint32_t)(align_up16(v1) - align_dn16(v0)) : 0u;
-    mbar_expect_tx(bar, bc + bm + br + bv);
-    bulk_g2s(slot, (const void *)align_dn16(c0), bc, bar, pol);
-    bulk_g2s(slot + lay.off_mask, (const void *)align_dn16(m0), bm, bar, pol);
-    if (br) bulk_g2s(slot + lay.off_rp, (const void *)align_dn16(r0), br, bar, pol);
-    if (bv) bulk_g2s(slot + lay.off_val, (const void *)align_dn16(v0), bv, bar, pol);
-}
-
-template <int BYTES>
-__device__ __forceinline__ uint32_t lds_lane_mask(const uint8_t *p) {
-    if constexpr (BYTES == 1) return *p;
-    else if constexpr (BYTES == 2) return *reinterpret_cast<const uint16_t *>(p);
-    else return *reinterpret_cast<const uint32_t *>(p);
-}
-
-constexpr int kSlots = 2;  // stages in flight per warp
-
-// K2.  R rows per panel, G rows per lane, L = R/G lanes per block,
-// BW = 32/L blocks per window (windows aligned to global multiples of BW).
-// Each warp streams its chunks stage by stage through a private ring of
-// kSlots shared-memory slots filled by cp.async.bulk (TMA); the lanes only
-// touch HBM for the x gathers and the y stores.
-template <typename T, typename MT, int R, int G>
+// K2.  GENERIC=false: the fast pass (whole matrix, chunks without empty
+// panels).  GENERIC=true: chunks with empty panels (block_rowptr search) and
+// panel-range products (spc5_spmv_panels / spmv_parallel).
+template <typename T, typename MT, int R, bool GENERIC>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvArgs a) {
     constexpr int MB = (int)sizeof(MT);
-    constexpr int MBITS = 8 * MB;
-    constexpr int L = R / G;
-    constexpr int BW = 32 / L;
-    constexpr int LB = G * MB;  // mask bytes per lane
-    static_assert(LB <= 4, "a lane's masks must fit 32 bits");
-    constexpr int NP = (G * MBITS >= 32) ? 6 : (G * MBITS >= 16 ? 5 : 4);
-    constexpr int NB = 4;  // value slots per batch
+    constexpr int LB = R * MB;  // mask bytes per lane (<= 16)
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const int blk = lane / L;
-    const int sub = lane % L;
+    const unsigned lane_le = kFull >> (31 - lane);  // bits 0..lane
     const T *__restrict__ x = static_cast<const T *>(a.x);
     T *__restrict__ y = static_cast<T *>(a.y);
 
-    SlotLayout lay;
-    lay.off_mask = a.lay_mask;
-    lay.off_rp = a.lay_rp;
-    lay.off_val = a.lay_val;
-    lay.bytes = a.lay_bytes;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * kSlots;
-    uint8_t *slots = smem + 128 + (size_t)warp * kSlots * lay.bytes +
-                     (size_t)0;  // barriers live in the first 128 bytes
+    const uint32_t ring = smem_addr(smem) + 128 + (uint32_t)(warp * kSlots) * a.lay_bytes;
     if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < kSlots; ++i) mbar_init(bars + i, 1);
@@ -278,7 +329,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
         for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < a.num_empty;
              i += (int64_t)gridDim.x * blockDim.x) {
             const int64_t p = a.empty_panels[i];
-            if (p < a.p_lo || p >= a.p_hi) continue;
+            if (GENERIC && (p < a.p_lo || p >= a.p_hi)) continue;
 #pragma unroll
             for (int rr = 0; rr < R; ++rr)
                 if (p * R + rr < a.num_rows) y[p * R + rr] = T(0);
@@ -288,244 +339,179 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
     const uint64_t pol = evict_first_policy();
     Cursor prod, cons;
     prod.gi = blockIdx.x;
-    cursor_seek(a, prod, warp);
+    cursor_seek<GENERIC>(a, prod, warp);
     cons = prod;
-    // prologue: fill the ring
 #pragma unroll
     for (int i = 0; i < kSlots; ++i) {
         if (prod.valid) {
-            if (lane == 0)
-                issue_stage<T, MT, R>(a, stage_desc(a, prod.c, prod.j), slots + i * lay.bytes, lay,
-                                      bars + i, pol);
-            cursor_next(a, prod, warp);
+            if (lane == 0) issue_chunk<T, LB>(a, prod.c, ring + i * a.lay_bytes, bars + i, pol);
+            prod.gi += gridDim.x;
+            cursor_seek<GENERIC>(a, prod, warp);
         }
     }
 
-    uint32_t it = 0;  // stages consumed by this warp
-    int64_t cur_chunk = -1;
-    double carry[G];
-    int64_t carry_panel = -1;
-    int64_t pc = 0;
+    uint32_t it = 0;
     while (cons.valid) {
         const int slot_i = it % kSlots;
         const uint32_t parity = (it / kSlots) & 1u;
-        uint8_t *slot = slots + slot_i * lay.bytes;
         const int64_t c = cons.c;
-        const StageDesc d = stage_desc(a, c, cons.j);
-        const int64_t cb0 = a.chunk_b[c], cb1 = a.chunk_b[c + 1];
-        const int64_t b0 = max(cb0, a.b_lo), b1 = min(cb1, a.b_hi);
+        const int64_t b0 = a.chunk_b[c], b1 = a.chunk_b[c + 1];
+        const int64_t v0 = a.chunk_v[c];
         const int64_t p0 = a.chunk_p[c];
-        if (c != cur_chunk) {  // chunk entry: fresh reduction state
-            cur_chunk = c;
-#pragma unroll
-            for (int g = 0; g < G; ++g) carry[g] = 0.0;
-            carry_panel = -1;
+        const uint8_t flags = a.chunk_flags[c];
+        const bool head_mid = flags & 1;  // first block continues a panel of earlier chunks
+        const int n = (int)(b1 - b0);
+        int a0 = 0, a1 = n;  // blocks contributing to y
+        bool slow = false;
+        int64_t pe = 0;
+        if (GENERIC) {
+            a0 = (int)(max(b0, a.b_lo) - b0);
+            a1 = (int)(min(b1, a.b_hi) - b0);
+            slow = flags & 2;
+            pe = a.chunk_p[c + 1];
         }
-        pc = d.p_s;
-        const bool head_mid = __ldg(a.rowptr + p0) < cb0;  // chunk starts inside panel p0
-        // element offsets of the stage inside its (16-byte widened) slot regions
-        const uint32_t *s_col = reinterpret_cast<const uint32_t *>(slot) +
-                                (((uint64_t)(a.colidx + d.start) & 15u) >> 2);
-        const uint8_t *s_mask = slot + lay.off_mask +
-                                ((uint64_t)((const uint8_t *)a.masks + d.start * R * MB) & 15u);
-        const int64_t rp_last = min(d.p_e + 1, a.num_panels);
-        const bool rp_staged = rp_last - d.p_s + 1 <= a.rp_cap;
-        const int64_t *s_rp = rp_staged ? reinterpret_cast<const int64_t *>(slot + lay.off_rp) +
-                                              (((uint64_t)(a.rowptr + d.p_s) & 15u) >> 3)
-                                        : a.rowptr + d.p_s;
-        const int n_rp = (int)(rp_last - d.p_s + 1);
-        const T *s_val = reinterpret_cast<const T *>(slot + lay.off_val) +
-                         (((uint64_t)((const T *)a.values + d.v_s) & 15u) / sizeof(T));
-        const int64_t wfirst = d.start - ((d.start + a.base_mod) % BW);
-        const int64_t cstart = max(cb0, d.start);  // first counted block of this stage
+        const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
+        // arrays are 256-byte aligned: a region's offset in its slot is its start mod 16
+        const uint32_t a_bits = sbase + (uint32_t)((((b0 + a.off32) >> 5) * 4) & 15);
+        const uint32_t a_col = sbase + a.lay_col + (uint32_t)((b0 * 4) & 15);
+        const uint32_t a_mask = sbase + a.lay_mask + (uint32_t)((b0 * LB) & 15);
+        const uint32_t a_val = sbase + a.lay_val + (uint32_t)((v0 * (int64_t)sizeof(T)) & 15);
+        const int sh0 = (int)((b0 + a.off32) & 31);
+
+        double carry[R];
+        bool carry_valid = false;
+        int carry_panel = 0;           // relative to p0
+        int pcur = head_mid ? 0 : -1;  // panel (rel. p0) of the block before the window
         uint32_t vrel = 0;
 
         mbar_wait(bars + slot_i, parity);
 
-        for (int64_t wb = wfirst; wb < d.end; wb += BW) {
-            const int64_t wn = wb + BW;
-            const bool last = wn >= b1;
-            const int64_t b = wb + blk;
-            const bool counted = b >= cstart && b < d.end;
-            const bool act = counted && b >= b0 && b < b1;
-            const int irel = (int)(b - d.start);
-            uint32_t col = 0, fm = 0;
-            if (counted) {
-                col = s_col[irel];
-                fm = lds_lane_mask<LB>(s_mask + (irel * R + sub * G) * MB);
+        for (int w = -sh0; w < a1; w += 32) {
+            const bool last = w + 32 >= a1;
+            const int br = w + lane;  // block relative to the chunk start
+            const bool counted = (unsigned)br < (unsigned)n;
+            const bool act = GENERIC ? (br >= a0 && br < a1) : counted;
+            const int bc = min(max(br, 0), n - 1);  // clamped: loads need no branch
+            const uint32_t col = lds_u32(a_col + (uint32_t)bc * 4u);
+            LaneMasks<LB> mk;
+            mk.load(a_mask + (uint32_t)bc * LB);
+            mk.clear_if(counted);
+            const int cnt = mk.popc();  // counted blocks advance the value cursor
+            const int incl = warp_incl_scan(cnt);
+            const int total = __shfl_sync(kFull, incl, 31);
+            // ---- panel starts in this window
+            uint32_t W = lds_u32(a_bits + (uint32_t)((sh0 + w) >> 5) * 4u);
+            if (w < 0 || n - w < 32) {  // first / last window: counted blocks only
+                const int lo_i = max(-w, 0), hi_i = min(n - w, 32);
+                W &= (hi_i >= 32 ? kFull : ((1u << hi_i) - 1u)) & ~((1u << lo_i) - 1u);
             }
-            // ---- issue the x gathers and value reads first (latency overlap)
-            const int cnt = __popc(fm);
-            const int cmax = __reduce_max_sync(kFull, act ? cnt : 0);
-            int excl, total;
-            warp_prefix<NP>(cnt, lane, excl, total);
-            T vv[NB], xv[NB];
-            int gsel[NB];
-            uint32_t fmc = act ? fm : 0u;
-            const T *xp = x + col;
-            const T *vp = s_val + vrel + excl;
-#pragma unroll
-            for (int u = 0; u < NB; ++u) {
-                const bool valid = fmc != 0u;
-                const int pos = __ffs(fmc) - 1;
-                fmc &= fmc - 1u;
-                gsel[u] = valid ? (G == 1 ? 0 : pos / MBITS) : -1;
-                if (valid) {
-                    xv[u] = __ldg(xp + (pos & (MBITS - 1)));
-                    vv[u] = vp[u];
+            // lanes past the active range form their own segment (appending zero
+            // lanes to a panel's segment would change the association of its sum)
+            const unsigned sent = (a1 - w < 32) ? (1u << (a1 - w)) : 0u;
+            int pl;  // panel relative to p0
+            unsigned hbits;
+            if (!GENERIC || !slow) {
+                pl = pcur + __popc(W & lane_le);
+                hbits = W | sent | 1u;
+                pcur += __popc(W);
+            } else {  // empty panels inside the chunk: search block_rowptr
+                const int64_t bq = b0 + max(br, 0);
+                int64_t lo = p0, hi = min(pe, a.num_panels - 1);
+                while (lo < hi) {
+                    const int64_t mid = lo + (hi - lo + 1) / 2;
+                    if (__ldg(a.rowptr + mid) <= bq) lo = mid;
+                    else hi = mid - 1;
                 }
-            }
-            // ---- panel of each block (block-level start bits) from the staged rowptr
-            const int pk = (int)(pc - d.p_s) + 1 + lane;
-            const int64_t E = pk < n_rp ? s_rp[pk] : INT64_MAX;
-            const int64_t dd64 = E - wb;
-            const bool in = dd64 >= 1 && dd64 < BW;
-            unsigned starts = __reduce_or_sync(kFull, in ? (1u << (int)dd64) : 0u);
-            const int nin = __popc(__ballot_sync(kFull, in));
-            int64_t pl, pend_last;
-            const unsigned blk_le = (BW == 32 && blk == 31) ? kFull : ((2u << blk) - 1u);
-            if (__popc(starts) == nin) {  // no empty panel inside the window
-                pl = pc + __popc(starts & blk_le);
-                pend_last = __shfl_sync(kFull, E, __popc(starts));
-            } else {  // empty panels: per-lane search over the loaded ends
-                const int64_t bq = max(b, cb0);
-                int cp = 0;
-#pragma unroll
-                for (int s2 = 16; s2 >= 1; s2 >>= 1) {
-                    const int64_t e = __shfl_sync(kFull, E, cp + s2 - 1);
-                    if (e <= bq) cp += s2;
-                }
-                const int64_t e31 = __shfl_sync(kFull, E, 31);
-                pl = pc + cp;
-                if (cp == 31 && e31 <= bq) {
-                    int64_t lo = pc, hi = a.num_panels;
-                    while (lo < hi) {
-                        const int64_t mid = lo + (hi - lo + 1) / 2;
-                        if (__ldg(a.rowptr + mid) <= bq) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    pl = lo;
-                }
-                const int64_t pprev = __shfl_up_sync(kFull, pl, L);
-                const unsigned hb = __ballot_sync(kFull, sub == 0 && blk > 0 && pl != pprev);
-                starts = 0;
-#pragma unroll
-                for (int t = 1; t < BW; ++t) starts |= ((hb >> (t * L)) & 1u) << t;
-                const int64_t pl_last = __shfl_sync(kFull, pl, 31);
-                pend_last = __ldg(a.rowptr + pl_last + 1);
-            }
-            // blocks past the chunk/range end: their own (silent) segment
-            if (b1 - wb < BW) starts |= 1u << (int)(b1 - wb);
-            const unsigned hbits = starts | 1u;
-            // next window's first panel
-            int64_t pcn = pc;
-            if (!last && wn < d.end) {
-                const int cn = __popc(__ballot_sync(kFull, E <= wn));
-                if (cn < 32) {
-                    pcn = pc + cn;
-                } else {
-                    int64_t lo = pc, hi = a.num_panels;
-                    while (lo < hi) {
-                        const int64_t mid = lo + (hi - lo + 1) / 2;
-                        if (__ldg(a.rowptr + mid) <= wn) lo = mid;
-                        else hi = mid - 1;
-                    }
-                    pcn = lo;
-                }
+                pl = (int)(lo - p0);
+                const int pprev = __shfl_up_sync(kFull, pl, 1);
+                hbits = __ballot_sync(kFull, lane > 0 && pl != pprev) | sent | 1u;
             }
 
-            // ---- products
-            double acc[G];
+            // ---- products: each panel row of the lane's block
+            double acc[R];
+            const T *xcol = x + col;
+            uint32_t vaddr = a_val + (vrel + (uint32_t)(incl - cnt)) * (uint32_t)sizeof(T);
 #pragma unroll
-            for (int g = 0; g < G; ++g) acc[g] = 0.0;
-#pragma unroll
-            for (int u = 0; u < NB; ++u) {
-                if (G == 1) {
-                    if (gsel[u] == 0) acc[0] = mul_acc<T>(acc[0], vv[u], xv[u]);
-                } else if (gsel[u] >= 0) {
-                    const double p = mul_acc<T>(0.0, vv[u], xv[u]);
-#pragma unroll
-                    for (int g = 0; g < G; ++g) acc[g] += (gsel[u] == g) ? p : 0.0;
-                }
-            }
-            for (int j0 = NB; j0 < cmax; j0 += NB) {  // dense blocks: more batches
-#pragma unroll
-                for (int u = 0; u < NB; ++u) {
-                    const bool valid = fmc != 0u;
-                    const int pos = __ffs(fmc) - 1;
-                    fmc &= fmc - 1u;
-                    gsel[u] = valid ? (G == 1 ? 0 : pos / MBITS) : -1;
-                    if (valid) {
-                        xv[u] = __ldg(xp + (pos & (MBITS - 1)));
-                        vv[u] = vp[j0 + u];
+            for (int g = 0; g < R; ++g) {
+                const uint32_t mrow = mk.template row<MB>(g);
+                uint32_t m = act ? mrow : 0u;
+                const int cg = __popc(m);
+                int hi = cg;
+                acc[g] = 0.0;
+                const int cmax = __reduce_max_sync(kFull, cg);
+                if (cmax > 0) {
+                    if (cmax <= 2) {
+                        row_slots<T, 2>(acc[g], m, hi, xcol, vaddr);
+                    } else if (cmax <= 4) {
+                        row_slots<T, 4>(acc[g], m, hi, xcol, vaddr);
+                    } else {
+                        for (int done = 0; done < cmax; done += 4)
+                            row_slots<T, 4>(acc[g], m, hi, xcol, vaddr);
                     }
                 }
-#pragma unroll
-                for (int u = 0; u < NB; ++u) {
-                    if (G == 1) {
-                        if (gsel[u] == 0) acc[0] = mul_acc<T>(acc[0], vv[u], xv[u]);
-                    } else if (gsel[u] >= 0) {
-                        const double p = mul_acc<T>(0.0, vv[u], xv[u]);
-#pragma unroll
-                        for (int g = 0; g < G; ++g) acc[g] += (gsel[u] == g) ? p : 0.0;
-                    }
-                }
+                vaddr += (uint32_t)__popc(mrow) * (uint32_t)sizeof(T);
             }
             vrel += (uint32_t)total;
-            if (blk == 0 && pl == carry_panel) {
+
+            // ---- the panel carried from the previous window: add or flush
+            if (carry_valid) {
+                const bool continues = __shfl_sync(kFull, pl, 0) == carry_panel;
+                if (lane == 0) {
+                    if (continues) {
 #pragma unroll
-                for (int g = 0; g < G; ++g) acc[g] += carry[g];
+                        for (int g = 0; g < R; ++g) acc[g] += carry[g];
+                    } else if (head_mid && carry_panel == 0) {
+#pragma unroll
+                        for (int g = 0; g < R; ++g) a.carry[c * R + g] = carry[g];
+                    } else {
+                        store_rows<T, R>(y, (p0 + carry_panel) * R, a.num_rows, carry,
+                                         a.accumulate);
+                    }
+                }
+                carry_valid = false;
             }
 
-            // ---- segmented scan over blocks of the same panel (stride L lanes)
-            const int segstart = 31 - __clz(hbits & blk_le);
+            // ---- segmented scan over lanes of the same panel
+            const int segstart = 31 - __clz(hbits & lane_le);
 #pragma unroll
-            for (int dd = 1; dd < BW; dd <<= 1) {
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const bool take = lane - dd >= segstart;
 #pragma unroll
-                for (int g = 0; g < G; ++g) {
-                    const double t = __shfl_up_sync(kFull, acc[g], dd * L);
-                    if (blk - dd >= segstart) acc[g] += t;
+                for (int g = 0; g < R; ++g) {
+                    const double t = __shfl_up_sync(kFull, acc[g], dd);
+                    if (take) acc[g] += t;
                 }
             }
-            const bool tailb = blk == BW - 1 || ((hbits >> (blk + 1)) & 1u);
-            const bool cont = pend_last > wn;  // last block's panel continues past the window
-            if (tailb && act && !(blk == BW - 1 && cont && !last) && pl >= a.p_lo &&
-                pl < a.p_hi) {
-                if (head_mid && pl == p0) {
+            const bool tail = lane == 31 || ((hbits >> (lane + 1)) & 1u);
+            // the window's last segment is carried unless the chunk ends here
+            if (tail && act && (lane != 31 || last)) {
+                if (head_mid && pl == 0) {
 #pragma unroll
-                    for (int g = 0; g < G; ++g) a.carry[c * R + sub * G + g] = acc[g];
+                    for (int g = 0; g < R; ++g) a.carry[c * R + g] = acc[g];
                 } else {
-#pragma unroll
-                    for (int g = 0; g < G; ++g) {
-                        const int64_t row = pl * R + sub * G + g;
-                        if (row < a.num_rows) {
-                            const T sv = (T)acc[g];
-                            y[row] = a.accumulate ? y[row] + sv : sv;
-                        }
-                    }
+                    store_rows<T, R>(y, (p0 + pl) * R, a.num_rows, acc, a.accumulate);
                 }
             }
             if (last) break;
-            // ---- carry into the next window
-            const int64_t pl_last = __shfl_sync(kFull, pl, 31);
 #pragma unroll
-            for (int g = 0; g < G; ++g) carry[g] = __shfl_sync(kFull, acc[g], (BW - 1) * L + sub);
-            carry_panel = cont ? pl_last : -1;
-            pc = pcn;
+            for (int g = 0; g < R; ++g) carry[g] = __shfl_sync(kFull, acc[g], 31);
+            carry_panel = __shfl_sync(kFull, pl, 31);
+            carry_valid = GENERIC ? __shfl_sync(kFull, act, 31) : true;
         }
 
-        // ---- release the slot and refill it with the stage kSlots ahead
+        // ---- release the slot and refill it with the chunk kSlots ahead
         __syncwarp();
         if (prod.valid) {
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_stage<T, MT, R>(a, stage_desc(a, prod.c, prod.j), slot, lay,
-                                      bars + slot_i, pol);
+                issue_chunk<T, LB>(a, prod.c, sbase, bars + slot_i, pol);
             }
-            cursor_next(a, prod, warp);
+            prod.gi += gridDim.x;
+            cursor_seek<GENERIC>(a, prod, warp);
         }
         ++it;
-        cursor_next(a, cons, warp);
+        cons.gi += gridDim.x;
+        cursor_seek<GENERIC>(a, cons, warp);
     }
 }
 
@@ -557,37 +543,57 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
     }
 }
 
-template <typename T, typename MT, int R, int G>
-int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
-    const size_t smem = 128 + (size_t)kWarpsPerCta * kSlots * a.lay_bytes;
-    static size_t smem_set = 0;
-    static int max_blocks_per_sm = 0;
-    if (smem > smem_set) {
-        SPC5_CUDA(cudaFuncSetAttribute(spmv_kernel<T, MT, R, G>,
-                                       cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-        smem_set = smem;
-        max_blocks_per_sm = 0;
-    }
-    static size_t occ_smem = 0;
-    if (!max_blocks_per_sm || occ_smem != smem) {
-        cudaOccupancyMaxActiveBlocksPerMultiprocessor(&max_blocks_per_sm,
-                                                      spmv_kernel<T, MT, R, G>,
-                                                      kWarpsPerCta * 32, smem);
-        if (max_blocks_per_sm < 1) max_blocks_per_sm = 1;
-        occ_smem = smem;
-    }
-    const int64_t nc = a.c_hi - a.c_lo;
-    int64_t grid = std::max<int64_t>(cdiv(std::max<int64_t>(nc, 1), kWarpsPerCta),
+template <typename K>
+int launch_ring_kernel(K kernel, const Matrix &m, const SpmvArgs &a, int64_t nslots,
+                       cudaStream_t st) {
+    const size_t smem = 128 + (size_t)kWarpsPerCta * kSlots * a.lay_bytes;  // barriers + ring
+    SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)smem));
+    int per_sm = 0;
+    SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarpsPerCta * 32,
+                                                            smem));
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = std::max<int64_t>(cdiv(std::max<int64_t>(nslots, 1), kWarpsPerCta),
                                      a.accumulate ? 1 : cdiv(a.num_empty, 256));
-    grid = std::min<int64_t>(grid, (int64_t)m.sm_count * max_blocks_per_sm);
+    grid = std::min<int64_t>(grid, (int64_t)m.sm_count * per_sm);
     grid = std::max<int64_t>(grid, 1);
-    spmv_kernel<T, MT, R, G><<<(unsigned)grid, kWarpsPerCta * 32, smem, st>>>(a);
+    kernel<<<(unsigned)grid, kWarpsPerCta * 32, smem, st>>>(a);
     SPC5_CUDA(cudaGetLastError());
-    int launches = 1;
-    if (m.plan.num_split) {
-        fixup_kernel<T, R><<<(unsigned)cdiv(m.plan.num_split, 128), 128, 0, st>>>(
-            m.plan.split_chunks, m.plan.num_split, m.plan.chunk_p, m.plan.carry,
-            static_cast<T *>(a.y), m.num_rows, a.c_lo, a.c_hi, a.p_lo, a.p_hi);
+    return SPC5_OK;
+}
+
+template <typename T, typename MT, int R>
+int launch_typed(const Matrix &m, const SpmvArgs &a0, cudaStream_t st) {
+    const Plan &P = m.plan;
+    int launches = 0;
+    const bool full = a0.p_lo == 0 && a0.p_hi == m.num_panels;
+    if (full) {
+        // fast pass over every chunk without empty panels, then the generic
+        // pass over the (usually empty) list of the others
+        SpmvArgs a = a0;
+        a.skip_generic = P.num_generic ? 1 : 0;
+        a.chunk_list = nullptr;
+        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false>, m, a, a.c_hi - a.c_lo, st));
+        ++launches;
+        if (P.num_generic) {
+            SpmvArgs g = a0;
+            g.chunk_list = P.generic_chunks;
+            g.c_lo = 0;
+            g.c_hi = P.num_generic;
+            g.num_empty = 0;  // zeroed by the fast pass
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, g, P.num_generic, st));
+            ++launches;
+        }
+    } else {
+        SpmvArgs g = a0;
+        g.chunk_list = nullptr;
+        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, g, g.c_hi - g.c_lo, st));
+        ++launches;
+    }
+    if (P.num_split) {
+        fixup_kernel<T, R><<<(unsigned)cdiv(P.num_split, 128), 128, 0, st>>>(
+            P.split_chunks, P.num_split, P.chunk_p, P.carry, static_cast<T *>(a0.y), m.num_rows,
+            a0.c_lo, a0.c_hi, a0.p_lo, a0.p_hi);
         SPC5_CUDA(cudaGetLastError());
         ++launches;
     }
@@ -597,14 +603,11 @@ int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
 
 template <typename T, typename MT>
 int dispatch_r(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
-    // G rows per lane: a lane's masks must fit 32 bits (G*sizeof(MT) <= 4)
-    constexpr int G2 = sizeof(MT) == 1 ? 2 : 2;
-    constexpr int G4 = sizeof(MT) == 1 ? 4 : 2;
     switch (m.r) {
-        case 1: return launch_typed<T, MT, 1, 1>(m, a, st);
-        case 2: return launch_typed<T, MT, 2, G2>(m, a, st);
-        case 4: return launch_typed<T, MT, 4, G4>(m, a, st);
-        default: return launch_typed<T, MT, 8, G4>(m, a, st);
+        case 1: return launch_typed<T, MT, 1>(m, a, st);
+        case 2: return launch_typed<T, MT, 2>(m, a, st);
+        case 4: return launch_typed<T, MT, 4>(m, a, st);
+        default: return launch_typed<T, MT, 8>(m, a, st);
     }
 }
 
@@ -625,24 +628,17 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
     a.chunk_b = P.chunk_b;
     a.chunk_v = P.chunk_v;
     a.chunk_p = P.chunk_p;
+    a.chunk_flags = P.chunk_flags;
+    a.pstart_bits = P.pstart_bits;
     a.carry = P.carry;
     a.empty_panels = P.empty_panels;
     a.num_empty = P.num_empty;
-    a.base_mod = (int)(((m.block_base % 32) + 32) % 32);  // windows divide 32
-    a.accumulate = accumulate;
-    a.stage_v = P.stage_v;
-    a.stage_p = P.stage_p;
-    a.stage_k = P.stage_granules;
     a.off32 = (int)(((m.block_base % 32) + 32) % 32);
-    a.rp_cap = P.rp_cap;
-    {
-        auto a16 = [](int64_t v) { return (uint32_t)((v + 15) / 16 * 16); };
-        const int64_t sb = 32LL * P.stage_granules;
-        a.lay_mask = a16(sb * 4 + 32);
-        a.lay_rp = a.lay_mask + a16(sb * m.r * m.mask_bytes() + 32);
-        a.lay_val = a.lay_rp + a16((int64_t)P.rp_cap * 8 + 32);
-        a.lay_bytes = (uint32_t)P.slot_bytes;
-    }
+    a.accumulate = accumulate;
+    a.lay_col = (uint32_t)P.lay_col;
+    a.lay_mask = (uint32_t)P.lay_mask;
+    a.lay_val = (uint32_t)P.lay_val;
+    a.lay_bytes = (uint32_t)P.slot_bytes;
     a.p_lo = p_lo;
     a.p_hi = p_hi;
     if (p_lo == 0 && p_hi == m.num_panels) {
