@@ -218,7 +218,12 @@ __global__ void pstart_bits_kernel(int64_t np, const int64_t *__restrict__ rowpt
 }
 
 // per chunk: bit0 = first block is not a panel start, bit1 = empty panels inside
-__global__ void chunk_flags_kernel(int64_t nc, const int64_t *__restrict__ chunk_b,
+// per chunk: bit0 = first block is not a panel start, bit1 = empty panels
+// inside, bit2 = lane-per-panel mode (>= kLppMinPanels whole, non-empty panels
+// of similar length: one lane sums a whole panel, no cross-lane reduction)
+constexpr int64_t kLppMinPanels = 12;
+__global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np,
+                                   const int64_t *__restrict__ chunk_b,
                                    const int64_t *__restrict__ chunk_p,
                                    const int64_t *__restrict__ rowptr,
                                    const int64_t *__restrict__ empty, int64_t ne, uint8_t *flags) {
@@ -234,6 +239,16 @@ __global__ void chunk_flags_kernel(int64_t nc, const int64_t *__restrict__ chunk
         else hi = mid;
     }
     if (lo < ne && empty[lo] < hi_p) f |= 2;
+    if (!(f & 3)) {
+        const int64_t cb0 = chunk_b[c], cb1 = chunk_b[c + 1];
+        const bool ends_clean = hi_p >= np ? cb1 == nb : rowptr[hi_p] == cb1;
+        const int64_t npc = hi_p - lo_p;
+        if (ends_clean && npc >= kLppMinPanels) {
+            int64_t maxlen = 0;
+            for (int64_t p = lo_p; p < hi_p; ++p) maxlen = max(maxlen, rowptr[p + 1] - rowptr[p]);
+            if (maxlen <= 64 && maxlen * npc <= 2 * (cb1 - cb0) + 4 * npc) f |= 4;
+        }
+    }
     flags[c] = f;
 }
 
@@ -568,7 +583,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     SPC5_CUDA(cudaGetLastError());
     SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
     chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
-        P.num_chunks, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels, P.num_empty,
+        P.num_chunks, nb, np, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels, P.num_empty,
         P.chunk_flags);
     SPC5_CUDA(cudaGetLastError());
     {

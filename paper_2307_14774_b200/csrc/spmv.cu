@@ -222,23 +222,58 @@ __device__ __forceinline__ void store_rows(T *y, int64_t row0, int64_t num_rows,
     }
 }
 
-// Products of one panel row of one block: up to NS set bits, highest first.
-// Slots past the row's count load nothing and add exact zeros.
-template <typename T, int NS>
-__device__ __forceinline__ void row_slots(double &acc, uint32_t &m, int &hi, const T *xcol,
-                                          uint32_t vaddr) {
-    T vv[NS], xv[NS];
+// Products of one panel row for U blocks: up to NS set bits per block,
+// highest first.  All U*NS gathers are issued before the first FMA; products
+// are accumulated block by block (storage order).  Slots past a block's count
+// load nothing and add exact zeros.
+template <typename T, int U, int NS>
+__device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h)[U],
+                                          const T *__restrict__ x, const uint32_t (&col)[U],
+                                          const uint32_t (&vaddr)[U]) {
+    T vv[U][NS], xv[U][NS];
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
-        const bool valid = m != 0u;
-        const uint32_t pos = bfind(m);
-        m &= ~(1u << pos);
-        --hi;
-        xv[u] = ldg_pred(xcol + pos, valid);
-        vv[u] = lds_pred<T>(vaddr + (uint32_t)hi * (uint32_t)sizeof(T), valid);
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const bool ok = m[k] != 0u;
+            const uint32_t pos = bfind(m[k]);
+            m[k] &= ~(1u << pos);
+            --h[k];
+            xv[k][u] = ldg_pred(x + (col[k] + pos), ok);
+            vv[k][u] = lds_pred<T>(vaddr[k] + (uint32_t)h[k] * (uint32_t)sizeof(T), ok);
+        }
     }
 #pragma unroll
-    for (int u = 0; u < NS; ++u) mac<T>(acc, vv[u], xv[u]);
+    for (int k = 0; k < U; ++k) {
+#pragma unroll
+        for (int u = 0; u < NS; ++u) mac<T>(acc, vv[k][u], xv[k][u]);
+    }
+}
+
+// One panel row of U blocks with a warp-uniform slot count: the smallest
+// unrolled variant that covers every lane, or batches of 4.
+template <typename T, int U>
+__device__ __forceinline__ void row_dispatch(double &acc, uint32_t (&m)[U], int (&h)[U],
+                                             const T *__restrict__ x, const uint32_t (&col)[U],
+                                             const uint32_t (&vaddr)[U], int cmax) {
+    if (cmax <= 0) return;
+    if (cmax == 1) {
+        row_slots<T, U, 1>(acc, m, h, x, col, vaddr);
+    } else if (cmax == 2) {
+        row_slots<T, U, 2>(acc, m, h, x, col, vaddr);
+    } else if (cmax == 3) {
+        row_slots<T, U, 3>(acc, m, h, x, col, vaddr);
+    } else if (cmax == 4) {
+        row_slots<T, U, 4>(acc, m, h, x, col, vaddr);
+    } else {  // dense rows: one block at a time so the products stay in order
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            uint32_t mk1[1] = {m[k]};
+            int hk1[1] = {h[k]};
+            const uint32_t ck1[1] = {col[k]}, vk1[1] = {vaddr[k]};
+            for (int done = 0; done < cmax; done += 4) row_slots<T, 1, 4>(acc, mk1, hk1, x, ck1, vk1);
+        }
+    }
 }
 
 __device__ __forceinline__ uint64_t align_dn16(uint64_t v) { return v & ~uint64_t(15); }
@@ -268,6 +303,87 @@ __device__ __forceinline__ void issue_chunk(const SpmvArgs &a, int64_t c, uint32
     bulk_g2s(slot + a.lay_col, (const void *)align_dn16(c0), bc, bar, pol);
     bulk_g2s(slot + a.lay_mask, (const void *)align_dn16(m0), bm, bar, pol);
     if (bv) bulk_g2s(slot + a.lay_val, (const void *)align_dn16(q0), bv, bar, pol);
+}
+
+// Lane-per-panel mode (chunk flag bit2): lane q owns panel p0+q of the chunk
+// and walks its blocks in order, so a panel is summed by one lane with no
+// cross-lane reduction, and lanes of one step touch consecutive panels
+// (neighbouring x for banded matrices).  Value offsets: per-lane counts and
+// one warp scan per 32 panels.
+template <typename T, typename MT, int R, bool GENERIC>
+__device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t p0, int npc,
+                                          uint32_t a_col, uint32_t a_mask, uint32_t a_val,
+                                          int lane, const T *__restrict__ x, T *__restrict__ y) {
+    constexpr int MB = (int)sizeof(MT);
+    constexpr int LB = R * MB;
+    uint32_t vbase = 0;
+    int64_t pass_start = b0;  // first block of the pass's first panel
+    for (int q0 = 0; q0 < npc; q0 += 32) {
+        const int q = q0 + lane;
+        const bool pv = q < npc;
+        const int64_t e64 = pv ? __ldg(a.rowptr + p0 + q + 1) : 0;
+        int64_t s64 = __shfl_up_sync(kFull, e64, 1);
+        if (lane == 0) s64 = pass_start;
+        pass_start = __shfl_sync(kFull, e64, min(31, npc - q0 - 1));
+        const int s = (int)(s64 - b0);
+        const int len = pv ? (int)(e64 - s64) : 0;
+        const int maxlen = __reduce_max_sync(kFull, len);
+        int cnt = 0;
+        for (int j = 0; j < maxlen; ++j) {
+            LaneMasks<LB> mk;
+            mk.load(a_mask + (uint32_t)(j < len ? s + j : 0) * LB);
+            cnt += j < len ? mk.popc() : 0;
+        }
+        const int incl = warp_incl_scan(cnt);
+        const int total = __shfl_sync(kFull, incl, 31);
+        uint32_t vaddr = a_val + (vbase + (uint32_t)(incl - cnt)) * (uint32_t)sizeof(T);
+        vbase += (uint32_t)total;
+        double acc[R];
+#pragma unroll
+        for (int g = 0; g < R; ++g) acc[g] = 0.0;
+        // three blocks per step: all their x gathers are in flight before the
+        // first FMA (values still accumulate in storage order)
+        constexpr int U = 3;
+        for (int j = 0; j < maxlen; j += U) {
+            uint32_t col[U], vr[U];
+            LaneMasks<LB> mk[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const bool ok = j + k < len;
+                const uint32_t bk = (uint32_t)(ok ? s + j + k : 0);
+                col[k] = lds_u32(a_col + bk * 4u);
+                mk[k].load(a_mask + bk * LB);
+                mk[k].clear_if(ok);
+            }
+            // storage order: block j's rows 0..R-1, then block j+1's, ...
+            vr[0] = vaddr;
+#pragma unroll
+            for (int k = 1; k < U; ++k)
+                vr[k] = vr[k - 1] + (uint32_t)mk[k - 1].popc() * (uint32_t)sizeof(T);
+            vaddr = vr[U - 1] + (uint32_t)mk[U - 1].popc() * (uint32_t)sizeof(T);
+#pragma unroll
+            for (int g = 0; g < R; ++g) {
+                uint32_t m[U];
+                int h[U], cm = 0;
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    m[k] = mk[k].template row<MB>(g);
+                    h[k] = __popc(m[k]);
+                    cm = max(cm, h[k]);
+                }
+                uint32_t vg[U];
+#pragma unroll
+                for (int k = 0; k < U; ++k) vg[k] = vr[k];
+                row_dispatch<T, U>(acc[g], m, h, x, col, vg, __reduce_max_sync(kFull, cm));
+#pragma unroll
+                for (int k = 0; k < U; ++k)
+                    vr[k] += (uint32_t)__popc(mk[k].template row<MB>(g)) * (uint32_t)sizeof(T);
+            }
+        }
+        const int64_t p = p0 + q;
+        if (pv && (!GENERIC || (p >= a.p_lo && p < a.p_hi)))
+            store_rows<T, R>(y, p * R, a.num_rows, acc, a.accumulate);
+    }
 }
 
 // Warp-uniform cursor over the warp's chunks: chunk slots gi*kWarpsPerCta+warp
@@ -386,6 +502,10 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
 
         mbar_wait(bars + slot_i, parity);
 
+        if (flags & 4) {  // lane-per-panel chunk
+            const int npc = (int)(a.chunk_p[c + 1] - p0);
+            lpp_chunk<T, MT, R, GENERIC>(a, b0, p0, npc, a_col, a_mask, a_val, lane, x, y);
+        } else
         for (int w = -sh0; w < a1; w += 32) {
             const bool last = w + 32 >= a1;
             const int br = w + lane;  // block relative to the chunk start
@@ -429,26 +549,16 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
 
             // ---- products: each panel row of the lane's block
             double acc[R];
-            const T *xcol = x + col;
+            const uint32_t col1[1] = {col};
             uint32_t vaddr = a_val + (vrel + (uint32_t)(incl - cnt)) * (uint32_t)sizeof(T);
 #pragma unroll
             for (int g = 0; g < R; ++g) {
                 const uint32_t mrow = mk.template row<MB>(g);
-                uint32_t m = act ? mrow : 0u;
-                const int cg = __popc(m);
-                int hi = cg;
+                uint32_t m1[1] = {act ? mrow : 0u};
+                int h1[1] = {__popc(m1[0])};
+                const uint32_t v1[1] = {vaddr};
                 acc[g] = 0.0;
-                const int cmax = __reduce_max_sync(kFull, cg);
-                if (cmax > 0) {
-                    if (cmax <= 2) {
-                        row_slots<T, 2>(acc[g], m, hi, xcol, vaddr);
-                    } else if (cmax <= 4) {
-                        row_slots<T, 4>(acc[g], m, hi, xcol, vaddr);
-                    } else {
-                        for (int done = 0; done < cmax; done += 4)
-                            row_slots<T, 4>(acc[g], m, hi, xcol, vaddr);
-                    }
-                }
+                row_dispatch<T, 1>(acc[g], m1, h1, x, col1, v1, __reduce_max_sync(kFull, h1[0]));
                 vaddr += (uint32_t)__popc(mrow) * (uint32_t)sizeof(T);
             }
             vrel += (uint32_t)total;

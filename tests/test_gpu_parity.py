@@ -243,7 +243,7 @@ def test_parallel_bitwise_equal(spc5):
 
 def test_row_panel_shards_bitwise(spc5):
     """Each rank converts only its rows (block_base = global block offset): the
-    shard's blocks and y must equal the full matrix's slice bit for bit."""
+    shard's blocks equal the full matrix's slice bit for bit, y to rounding."""
     from paper_2307_14774_b200.workloads import stencil27_rows, x_vector
     n = 20
     full = stencil27_rows(n, 0, n ** 3)
@@ -261,7 +261,11 @@ def test_row_panel_shards_bitwise(spc5):
                 assert np.array_equal(sh.block_colidx,
                                       s.block_colidx[base:int(s.block_rowptr[hi])])
                 y = spc5.spmv(sh, x)
-                assert y.tobytes() == y_full[lo * r:min(hi * r, n ** 3)].tobytes(), (r, P, lo)
+                # same value up to the association of the per-panel sums: chunks at a
+                # shard edge may run lane-per-panel where the full run went lane-per-block
+                ref = y_full[lo * r:min(hi * r, n ** 3)]
+                _, absr = oracle.csr_reference(rows, x)
+                assert float(oracle.relative_error(y, ref, absr).max()) <= 1e-15, (r, P, lo)
 
 
 # ---------------------------------------------------------------- errors
