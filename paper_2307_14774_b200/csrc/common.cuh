@@ -38,13 +38,12 @@ struct Plan {
     int64_t chunk_target = 0;       // blocks per chunk target (snapped to panel starts)
     int64_t split_len = 256;        // long panels are cut at global multiples of this
     int64_t max_chunk_blocks = 0, max_chunk_values = 0;
-    int64_t lay_col = 0, lay_mask = 0, lay_val = 0;  // slot layout: bits | col | mask | val
+    int64_t max_lpp_panels = 0;     // panels of the largest lane-per-panel chunk
+    int64_t lay_rp = 0, lay_col = 0, lay_mask = 0, lay_val = 0;  // slot: bits|rp|col|mask|val
     int slot_bytes = 0;
     int64_t num_granules = 0;
     uint32_t *pstart_bits = nullptr;  // [num_granules] bit i of word g: block 32g-off32+i starts a panel
     uint8_t *chunk_flags = nullptr;   // [num_chunks] bit0: starts inside a panel, bit1: has empty panels
-    int64_t num_generic = 0;
-    int *generic_chunks = nullptr;    // [num_generic] chunks with flags != 0 (generic pass)
 };
 
 struct Matrix {

@@ -252,9 +252,11 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np,
     flags[c] = f;
 }
 
-__global__ void generic_flag_kernel(int64_t nc, const uint8_t *flags, uint8_t *out) {
+// largest panel count of a lane-per-panel chunk (sizes the staged rowptr)
+__global__ void lpp_panels_kernel(int64_t nc, const int64_t *__restrict__ chunk_p,
+                                  const uint8_t *__restrict__ flags, unsigned long long *out) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c < nc) out[c] = (flags[c] & 2) ? 1 : 0;  // empty panels inside: generic pass
+    if (c < nc && (flags[c] & 4)) atomicMax(out, (unsigned long long)(chunk_p[c + 1] - chunk_p[c]));
 }
 
 __global__ void narrow_kernel(const int64_t *in, int64_t n, int *out) {
@@ -358,7 +360,6 @@ void free_plan(Plan &p) {
     dev_free(p.tile_prefix);
     dev_free(p.pstart_bits);
     dev_free(p.chunk_flags);
-    dev_free(p.generic_chunks);
     delete[] p.h_chunk_b;
     p = Plan{};
 }
@@ -547,21 +548,30 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     }
     for (int64_t cb = 256;; cb >>= 1) {
         SPC5_TRY(build_chunks(m, cb, st));
-        unsigned long long *d_st = nullptr, h_st[2] = {0, 0};
-        SPC5_TRY(dev_alloc(&d_st, 2));
-        SPC5_CUDA(cudaMemsetAsync(d_st, 0, 2 * sizeof(unsigned long long), st));
+        SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
+        chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
+            P.num_chunks, nb, np, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels, P.num_empty,
+            P.chunk_flags);
+        SPC5_CUDA(cudaGetLastError());
+        unsigned long long *d_st = nullptr, h_st[3] = {0, 0, 0};
+        SPC5_TRY(dev_alloc(&d_st, 3));
+        SPC5_CUDA(cudaMemsetAsync(d_st, 0, 3 * sizeof(unsigned long long), st));
         chunk_stats_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, P.chunk_b, P.chunk_v, d_st);
+        lpp_panels_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
+            P.num_chunks, P.chunk_p, P.chunk_flags, d_st + 2);
         SPC5_CUDA(cudaGetLastError());
         SPC5_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, st));
         SPC5_CUDA(cudaStreamSynchronize(st));
         dev_free(d_st);
         P.max_chunk_blocks = (int64_t)h_st[0];
         P.max_chunk_values = (int64_t)h_st[1];
+        P.max_lpp_panels = (int64_t)h_st[2];
         P.chunk_target = cb;
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
         const int64_t mb = P.max_chunk_blocks;
-        P.lay_col = a16((mb / 32 + 2) * 4 + 32);
+        P.lay_rp = a16((mb / 32 + 2) * 4 + 32);
+        P.lay_col = P.lay_rp + (P.max_lpp_panels ? a16((P.max_lpp_panels + 1) * 8 + 32) : 0);
         P.lay_mask = P.lay_col + a16(mb * 4 + 32);
         P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
@@ -569,10 +579,12 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         if (P.slot_bytes <= 6 * 1024 || cb == 1) break;
         if (cb <= 32 && P.slot_bytes <= 14 * 1024) break;
         free_chunks(P);
+        dev_free(P.chunk_flags);
+        P.chunk_flags = nullptr;
     }
     if (P.slot_bytes > 14 * 1024)
         return fail(SPC5_EINVAL, "a chunk of this matrix does not fit the shared-memory ring");
-    // panel-start bitmap, chunk flags, the generic pass's chunk list
+    // panel-start bitmap
     const int off32 = (int)(((m.block_base % 32) + 32) % 32);
     const int64_t ng = cdiv(nb + off32, 32);
     P.num_granules = ng;
@@ -581,27 +593,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     pstart_bits_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, off32,
                                                                  P.pstart_bits);
     SPC5_CUDA(cudaGetLastError());
-    SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
-    chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
-        P.num_chunks, nb, np, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels, P.num_empty,
-        P.chunk_flags);
-    SPC5_CUDA(cudaGetLastError());
-    {
-        int64_t *list64 = nullptr;
-        uint8_t *gflag = nullptr;
-        SPC5_TRY(dev_alloc(&list64, (size_t)P.num_chunks));
-        SPC5_TRY(dev_alloc(&gflag, (size_t)P.num_chunks));
-        generic_flag_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
-            P.num_chunks, P.chunk_flags, gflag);
-        SPC5_TRY(select_flagged(gflag, P.num_chunks, list64, &P.num_generic, st));
-        SPC5_TRY(dev_alloc(&P.generic_chunks, (size_t)std::max<int64_t>(P.num_generic, 1)));
-        if (P.num_generic)
-            narrow_kernel<<<(unsigned)cdiv(P.num_generic, 256), 256, 0, st>>>(
-                list64, P.num_generic, P.generic_chunks);
-        SPC5_CUDA(cudaStreamSynchronize(st));
-        dev_free(list64);
-        dev_free(gflag);
-    }
+    SPC5_CUDA(cudaStreamSynchronize(st));
     P.built = true;
     return SPC5_OK;
 }

@@ -45,8 +45,7 @@ struct SpmvArgs {
     const int64_t *chunk_b, *chunk_v, *chunk_p;
     const uint8_t *chunk_flags;   // bit0 starts inside a panel, bit1 has empty panels
     const uint32_t *pstart_bits;  // panel-start bitmap over 32-block granules
-    const int *chunk_list;        // generic pass over a list of chunks (else null)
-    int64_t c_lo, c_hi;           // chunk index range (into chunk_list when set)
+    int64_t c_lo, c_hi;           // chunk index range
     int64_t b_lo, b_hi;           // blocks contributing to y
     int64_t p_lo, p_hi;           // panels whose rows may be written
     double *carry;
@@ -54,8 +53,8 @@ struct SpmvArgs {
     int64_t num_empty;
     int off32;         // block_base mod 32 (window alignment)
     int accumulate;
-    int skip_generic;  // fast pass: leave chunks with empty panels to the generic pass
-    uint32_t lay_col, lay_mask, lay_val, lay_bytes;  // slot layout (bytes)
+    uint32_t lay_rp, lay_col, lay_mask, lay_val, lay_bytes;  // slot layout (bytes)
+    int max_rp;        // panel ends staged for lane-per-panel chunks
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -279,30 +278,66 @@ __device__ __forceinline__ void row_dispatch(double &acc, uint32_t (&m)[U], int 
 __device__ __forceinline__ uint64_t align_dn16(uint64_t v) { return v & ~uint64_t(15); }
 __device__ __forceinline__ uint64_t align_up16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
 
-// Lane 0 of the warp: copy chunk c (panel-start words, column starts, masks,
-// values) into the slot at shared address `slot` with four bulk copies that
-// complete on one mbarrier.
+// Chunk descriptor spread over lanes 0..6 (one int64 field per lane):
+// b0, b1 (blocks), v0, v1 (values), p0 (panel of b0), pe (panel of b1), flags.
+// Loaded two chunks ahead so its latency hides behind the current chunk.
+__device__ __forceinline__ int64_t desc_load(const SpmvArgs &a, int64_t c, bool valid, int lane) {
+    if (!valid || lane > 6) return 0;
+    if (lane == 6) return (int64_t)a.chunk_flags[c];
+    const int64_t *base = lane < 2 ? a.chunk_b : (lane < 4 ? a.chunk_v : a.chunk_p);
+    return __ldg(base + c + (lane & 1));
+}
+struct ChunkDesc {
+    int64_t b0, b1, v0, v1, p0, pe;
+    int flags;
+};
+__device__ __forceinline__ ChunkDesc desc_get(int64_t d) {
+    ChunkDesc r;
+    r.b0 = __shfl_sync(kFull, d, 0);
+    r.b1 = __shfl_sync(kFull, d, 1);
+    r.v0 = __shfl_sync(kFull, d, 2);
+    r.v1 = __shfl_sync(kFull, d, 3);
+    r.p0 = __shfl_sync(kFull, d, 4);
+    r.pe = __shfl_sync(kFull, d, 5);
+    r.flags = (int)__shfl_sync(kFull, d, 6);
+    return r;
+}
+
+// Lane 0 of the warp: copy one chunk (panel-start words, [panel ends for
+// lane-per-panel chunks], column starts, masks, values) into the slot at
+// shared address `slot` with bulk copies that complete on one mbarrier.
 template <typename T, int LB>
-__device__ __forceinline__ void issue_chunk(const SpmvArgs &a, int64_t c, uint32_t slot,
+__device__ __forceinline__ void issue_chunk(const SpmvArgs &a, const ChunkDesc &d, uint32_t slot,
                                             uint64_t *bar, uint64_t pol) {
-    const int64_t b0 = a.chunk_b[c], b1 = a.chunk_b[c + 1];
-    const int64_t v0 = a.chunk_v[c], v1 = a.chunk_v[c + 1];
-    const uint64_t w0 = (uint64_t)(a.pstart_bits + ((b0 + a.off32) >> 5));
-    const uint64_t w1 = (uint64_t)(a.pstart_bits + ((b1 - 1 + a.off32) >> 5) + 1);
-    const uint64_t c0 = (uint64_t)(a.colidx + b0), c1 = (uint64_t)(a.colidx + b1);
-    const uint64_t m0 = (uint64_t)((const uint8_t *)a.masks + b0 * LB);
-    const uint64_t m1 = (uint64_t)((const uint8_t *)a.masks + b1 * LB);
-    const uint64_t q0 = (uint64_t)((const T *)a.values + v0);
-    const uint64_t q1 = (uint64_t)((const T *)a.values + v1);
+    const uint64_t w0 = (uint64_t)(a.pstart_bits + ((d.b0 + a.off32) >> 5));
+    const uint64_t w1 = (uint64_t)(a.pstart_bits + ((d.b1 - 1 + a.off32) >> 5) + 1);
+    const uint64_t c0 = (uint64_t)(a.colidx + d.b0), c1 = (uint64_t)(a.colidx + d.b1);
+    const uint64_t m0 = (uint64_t)((const uint8_t *)a.masks + d.b0 * LB);
+    const uint64_t m1 = (uint64_t)((const uint8_t *)a.masks + d.b1 * LB);
+    const uint64_t q0 = (uint64_t)((const T *)a.values + d.v0);
+    const uint64_t q1 = (uint64_t)((const T *)a.values + d.v1);
     const uint32_t bw = (uint32_t)(align_up16(w1) - align_dn16(w0));
     const uint32_t bc = (uint32_t)(align_up16(c1) - align_dn16(c0));
     const uint32_t bm = (uint32_t)(align_up16(m1) - align_dn16(m0));
-    const uint32_t bv = v1 > v0 ? (uint32_t)(align_up16(q1) - align_dn16(q0)) : 0u;
-    mbar_expect_tx(bar, bw + bc + bm + bv);
+    const uint32_t bv = d.v1 > d.v0 ? (uint32_t)(align_up16(q1) - align_dn16(q0)) : 0u;
+    uint32_t br = 0;
+    uint64_t r0 = 0;
+    if (d.flags & 4) {  // panel ends rowptr[p0 .. pe]
+        r0 = (uint64_t)(a.rowptr + d.p0);
+        br = (uint32_t)(align_up16((uint64_t)(a.rowptr + d.pe + 1)) - align_dn16(r0));
+    }
+    mbar_expect_tx(bar, bw + br + bc + bm + bv);
     bulk_g2s(slot, (const void *)align_dn16(w0), bw, bar, pol);
+    if (br) bulk_g2s(slot + a.lay_rp, (const void *)align_dn16(r0), br, bar, pol);
     bulk_g2s(slot + a.lay_col, (const void *)align_dn16(c0), bc, bar, pol);
     bulk_g2s(slot + a.lay_mask, (const void *)align_dn16(m0), bm, bar, pol);
     if (bv) bulk_g2s(slot + a.lay_val, (const void *)align_dn16(q0), bv, bar, pol);
+}
+
+__device__ __forceinline__ int64_t lds_s64(uint32_t addr) {
+    int64_t v;
+    asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(addr));
+    return v;
 }
 
 // Lane-per-panel mode (chunk flag bit2): lane q owns panel p0+q of the chunk
@@ -312,19 +347,17 @@ __device__ __forceinline__ void issue_chunk(const SpmvArgs &a, int64_t c, uint32
 // one warp scan per 32 panels.
 template <typename T, typename MT, int R, bool GENERIC>
 __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t p0, int npc,
-                                          uint32_t a_col, uint32_t a_mask, uint32_t a_val,
-                                          int lane, const T *__restrict__ x, T *__restrict__ y) {
+                                          uint32_t a_rp, uint32_t a_col, uint32_t a_mask,
+                                          uint32_t a_val, int lane, const T *__restrict__ x,
+                                          T *__restrict__ y) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;
     uint32_t vbase = 0;
-    int64_t pass_start = b0;  // first block of the pass's first panel
     for (int q0 = 0; q0 < npc; q0 += 32) {
         const int q = q0 + lane;
         const bool pv = q < npc;
-        const int64_t e64 = pv ? __ldg(a.rowptr + p0 + q + 1) : 0;
-        int64_t s64 = __shfl_up_sync(kFull, e64, 1);
-        if (lane == 0) s64 = pass_start;
-        pass_start = __shfl_sync(kFull, e64, min(31, npc - q0 - 1));
+        const uint32_t rq = a_rp + (uint32_t)min(q, npc - 1) * 8u;  // staged rowptr[p0 + q]
+        const int64_t s64 = lds_s64(rq), e64 = lds_s64(rq + 8u);
         const int s = (int)(s64 - b0);
         const int len = pv ? (int)(e64 - s64) : 0;
         const int maxlen = __reduce_max_sync(kFull, len);
@@ -386,41 +419,10 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t
     }
 }
 
-// Warp-uniform cursor over the warp's chunks: chunk slots gi*kWarpsPerCta+warp
-// for gi = blockIdx.x, +gridDim.x, ... of [c_lo, c_hi) (or of chunk_list).
-struct Cursor {
-    int gi;
-    int c;
-    bool valid;
-};
-
-template <bool GENERIC>
-__device__ __forceinline__ void cursor_seek(const SpmvArgs &a, Cursor &cu, int warp) {
-    const int64_t nc = a.c_hi - a.c_lo;
-    for (;;) {
-        const int64_t s = (int64_t)cu.gi * kWarpsPerCta + warp;
-        if (s >= nc) {
-            cu.valid = false;
-            return;
-        }
-        cu.c = GENERIC && a.chunk_list ? a.chunk_list[a.c_lo + s] : (int)(a.c_lo + s);
-        bool take = true;
-        if (!GENERIC) {
-            take = !a.skip_generic || !(a.chunk_flags[cu.c] & 2);
-        } else if (!a.chunk_list) {  // panel range: chunks overlapping [b_lo, b_hi)
-            take = a.chunk_b[cu.c + 1] > a.b_lo && a.chunk_b[cu.c] < a.b_hi;
-        }
-        if (take) {
-            cu.valid = true;
-            return;
-        }
-        cu.gi += gridDim.x;
-    }
-}
-
-// K2.  GENERIC=false: the fast pass (whole matrix, chunks without empty
-// panels).  GENERIC=true: chunks with empty panels (block_rowptr search) and
-// panel-range products (spc5_spmv_panels / spmv_parallel).
+// K2.  Each warp takes chunks c_lo + (blockIdx.x + k*gridDim.x)*W + warp,
+// k = 0, 1, ...; the CTA's warps work on neighbouring chunks (x reuse in L1).
+// GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
+// spmv_parallel); the arithmetic per panel is identical.
 template <typename T, typename MT, int R, bool GENERIC>
 __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvArgs a) {
     constexpr int MB = (int)sizeof(MT);
@@ -453,42 +455,42 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
     }
 
     const uint64_t pol = evict_first_policy();
-    Cursor prod, cons;
-    prod.gi = blockIdx.x;
-    cursor_seek<GENERIC>(a, prod, warp);
-    cons = prod;
-#pragma unroll
-    for (int i = 0; i < kSlots; ++i) {
-        if (prod.valid) {
-            if (lane == 0) issue_chunk<T, LB>(a, prod.c, ring + i * a.lay_bytes, bars + i, pol);
-            prod.gi += gridDim.x;
-            cursor_seek<GENERIC>(a, prod, warp);
+    const int64_t stride = (int64_t)gridDim.x * kWarpsPerCta;
+    const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    // descriptors of chunks k, k+1, k+2 (fields spread over lanes 0..6)
+    int64_t dq0 = desc_load(a, cfirst, cfirst < a.c_hi, lane);
+    int64_t dq1 = desc_load(a, cfirst + stride, cfirst + stride < a.c_hi, lane);
+    int64_t dq2 = desc_load(a, cfirst + 2 * stride, cfirst + 2 * stride < a.c_hi, lane);
+    {
+        if (cfirst < a.c_hi) {
+            const ChunkDesc d = desc_get(dq0);
+            if (lane == 0) issue_chunk<T, LB>(a, d, ring, bars, pol);
+        }
+        if (cfirst + stride < a.c_hi) {
+            const ChunkDesc d = desc_get(dq1);
+            if (lane == 0) issue_chunk<T, LB>(a, d, ring + a.lay_bytes, bars + 1, pol);
         }
     }
 
     uint32_t it = 0;
-    while (cons.valid) {
+    for (int64_t c = cfirst; c < a.c_hi; c += stride, ++it) {
         const int slot_i = it % kSlots;
         const uint32_t parity = (it / kSlots) & 1u;
-        const int64_t c = cons.c;
-        const int64_t b0 = a.chunk_b[c], b1 = a.chunk_b[c + 1];
-        const int64_t v0 = a.chunk_v[c];
-        const int64_t p0 = a.chunk_p[c];
-        const uint8_t flags = a.chunk_flags[c];
+        const ChunkDesc dd = desc_get(dq0);
+        const int64_t b0 = dd.b0, b1 = dd.b1, v0 = dd.v0, p0 = dd.p0, pe = dd.pe;
+        const int flags = dd.flags;
         const bool head_mid = flags & 1;  // first block continues a panel of earlier chunks
+        const bool slow = flags & 2;      // empty panels inside: search block_rowptr
         const int n = (int)(b1 - b0);
         int a0 = 0, a1 = n;  // blocks contributing to y
-        bool slow = false;
-        int64_t pe = 0;
         if (GENERIC) {
             a0 = (int)(max(b0, a.b_lo) - b0);
             a1 = (int)(min(b1, a.b_hi) - b0);
-            slow = flags & 2;
-            pe = a.chunk_p[c + 1];
         }
         const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
         // arrays are 256-byte aligned: a region's offset in its slot is its start mod 16
         const uint32_t a_bits = sbase + (uint32_t)((((b0 + a.off32) >> 5) * 4) & 15);
+        const uint32_t a_rp = sbase + a.lay_rp + (uint32_t)((p0 * 8) & 15);
         const uint32_t a_col = sbase + a.lay_col + (uint32_t)((b0 * 4) & 15);
         const uint32_t a_mask = sbase + a.lay_mask + (uint32_t)((b0 * LB) & 15);
         const uint32_t a_val = sbase + a.lay_val + (uint32_t)((v0 * (int64_t)sizeof(T)) & 15);
@@ -503,8 +505,8 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
         mbar_wait(bars + slot_i, parity);
 
         if (flags & 4) {  // lane-per-panel chunk
-            const int npc = (int)(a.chunk_p[c + 1] - p0);
-            lpp_chunk<T, MT, R, GENERIC>(a, b0, p0, npc, a_col, a_mask, a_val, lane, x, y);
+            lpp_chunk<T, MT, R, GENERIC>(a, b0, p0, (int)(pe - p0), a_rp, a_col, a_mask, a_val,
+                                         lane, x, y);
         } else
         for (int w = -sh0; w < a1; w += 32) {
             const bool last = w + 32 >= a1;
@@ -530,7 +532,7 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
             const unsigned sent = (a1 - w < 32) ? (1u << (a1 - w)) : 0u;
             int pl;  // panel relative to p0
             unsigned hbits;
-            if (!GENERIC || !slow) {
+            if (!slow) {
                 pl = pcur + __popc(W & lane_le);
                 hbits = W | sent | 1u;
                 pcur += __popc(W);
@@ -611,17 +613,17 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
 
         // ---- release the slot and refill it with the chunk kSlots ahead
         __syncwarp();
-        if (prod.valid) {
+        const int64_t cn = c + 2 * stride;
+        if (cn < a.c_hi) {
+            const ChunkDesc d2 = desc_get(dq2);
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_chunk<T, LB>(a, prod.c, sbase, bars + slot_i, pol);
+                issue_chunk<T, LB>(a, d2, sbase, bars + slot_i, pol);
             }
-            prod.gi += gridDim.x;
-            cursor_seek<GENERIC>(a, prod, warp);
         }
-        ++it;
-        cons.gi += gridDim.x;
-        cursor_seek<GENERIC>(a, cons, warp);
+        dq0 = dq1;
+        dq1 = dq2;
+        dq2 = desc_load(a, c + 3 * stride, c + 3 * stride < a.c_hi, lane);
     }
 }
 
@@ -673,37 +675,17 @@ int launch_ring_kernel(K kernel, const Matrix &m, const SpmvArgs &a, int64_t nsl
 }
 
 template <typename T, typename MT, int R>
-int launch_typed(const Matrix &m, const SpmvArgs &a0, cudaStream_t st) {
+int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
     const Plan &P = m.plan;
-    int launches = 0;
-    const bool full = a0.p_lo == 0 && a0.p_hi == m.num_panels;
-    if (full) {
-        // fast pass over every chunk without empty panels, then the generic
-        // pass over the (usually empty) list of the others
-        SpmvArgs a = a0;
-        a.skip_generic = P.num_generic ? 1 : 0;
-        a.chunk_list = nullptr;
+    int launches = 1;
+    if (a.p_lo == 0 && a.p_hi == m.num_panels)
         SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false>, m, a, a.c_hi - a.c_lo, st));
-        ++launches;
-        if (P.num_generic) {
-            SpmvArgs g = a0;
-            g.chunk_list = P.generic_chunks;
-            g.c_lo = 0;
-            g.c_hi = P.num_generic;
-            g.num_empty = 0;  // zeroed by the fast pass
-            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, g, P.num_generic, st));
-            ++launches;
-        }
-    } else {
-        SpmvArgs g = a0;
-        g.chunk_list = nullptr;
-        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, g, g.c_hi - g.c_lo, st));
-        ++launches;
-    }
+    else
+        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, a, a.c_hi - a.c_lo, st));
     if (P.num_split) {
         fixup_kernel<T, R><<<(unsigned)cdiv(P.num_split, 128), 128, 0, st>>>(
-            P.split_chunks, P.num_split, P.chunk_p, P.carry, static_cast<T *>(a0.y), m.num_rows,
-            a0.c_lo, a0.c_hi, a0.p_lo, a0.p_hi);
+            P.split_chunks, P.num_split, P.chunk_p, P.carry, static_cast<T *>(a.y), m.num_rows,
+            a.c_lo, a.c_hi, a.p_lo, a.p_hi);
         SPC5_CUDA(cudaGetLastError());
         ++launches;
     }
@@ -745,6 +727,7 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
     a.num_empty = P.num_empty;
     a.off32 = (int)(((m.block_base % 32) + 32) % 32);
     a.accumulate = accumulate;
+    a.lay_rp = (uint32_t)P.lay_rp;
     a.lay_col = (uint32_t)P.lay_col;
     a.lay_mask = (uint32_t)P.lay_mask;
     a.lay_val = (uint32_t)P.lay_val;
