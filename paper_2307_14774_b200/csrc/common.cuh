@@ -18,7 +18,6 @@
 namespace spc5 {
 
 constexpr int kTile = 1024;       // blocks per popcount-prefix tile
-constexpr int kWarpsPerCta = 8;   // SpMV CTA = 8 warps, one chunk per warp
 
 struct Plan {
     bool built = false;

@@ -546,7 +546,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         while (sl > 1 && sl * max_block_bytes > 6 * 1024) sl >>= 1;
         P.split_len = sl;
     }
-    for (int64_t cb = 256;; cb >>= 1) {
+    for (int64_t cb = 512;; cb >>= 1) {
         SPC5_TRY(build_chunks(m, cb, st));
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
@@ -576,7 +576,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
                              128 * 128);
-        if (P.slot_bytes <= 6 * 1024 || cb == 1) break;
+        if (P.slot_bytes <= 10 * 1024 || cb == 1) break;
         if (cb <= 32 && P.slot_bytes <= 14 * 1024) break;
         free_chunks(P);
         dev_free(P.chunk_flags);

@@ -424,7 +424,7 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t
 // GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
 // spmv_parallel); the arithmetic per panel is identical.
 template <typename T, typename MT, int R, bool GENERIC>
-__global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvArgs a) {
+__global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;  // mask bytes per lane (<= 16)
     extern __shared__ __align__(128) uint8_t smem[];
@@ -455,8 +455,9 @@ __global__ void __launch_bounds__(kWarpsPerCta * 32, 2) spmv_kernel(const SpmvAr
     }
 
     const uint64_t pol = evict_first_policy();
-    const int64_t stride = (int64_t)gridDim.x * kWarpsPerCta;
-    const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * kWarpsPerCta + warp;
+    const int wpc = blockDim.x >> 5;  // warps per CTA
+    const int64_t stride = (int64_t)gridDim.x * wpc;
+    const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * wpc + warp;
     // descriptors of chunks k, k+1, k+2 (fields spread over lanes 0..6)
     int64_t dq0 = desc_load(a, cfirst, cfirst < a.c_hi, lane);
     int64_t dq1 = desc_load(a, cfirst + stride, cfirst + stride < a.c_hi, lane);
@@ -658,18 +659,19 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
 template <typename K>
 int launch_ring_kernel(K kernel, const Matrix &m, const SpmvArgs &a, int64_t nslots,
                        cudaStream_t st) {
-    const size_t smem = 128 + (size_t)kWarpsPerCta * kSlots * a.lay_bytes;  // barriers + ring
+    // 8 warps per CTA for small slots; 4 for large ones so several CTAs share an SM
+    const int wpc = a.lay_bytes <= 6 * 1024 ? 8 : 4;
+    const size_t smem = 128 + (size_t)wpc * kSlots * a.lay_bytes;  // barriers + ring
     SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     int per_sm = 0;
-    SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kWarpsPerCta * 32,
-                                                            smem));
+    SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, wpc * 32, smem));
     if (per_sm < 1) per_sm = 1;
-    int64_t grid = std::max<int64_t>(cdiv(std::max<int64_t>(nslots, 1), kWarpsPerCta),
+    int64_t grid = std::max<int64_t>(cdiv(std::max<int64_t>(nslots, 1), wpc),
                                      a.accumulate ? 1 : cdiv(a.num_empty, 256));
     grid = std::min<int64_t>(grid, (int64_t)m.sm_count * per_sm);
     grid = std::max<int64_t>(grid, 1);
-    kernel<<<(unsigned)grid, kWarpsPerCta * 32, smem, st>>>(a);
+    kernel<<<(unsigned)grid, wpc * 32, smem, st>>>(a);
     SPC5_CUDA(cudaGetLastError());
     return SPC5_OK;
 }
