@@ -219,10 +219,10 @@ __global__ void pstart_bits_kernel(int64_t np, const int64_t *__restrict__ rowpt
 
 // per chunk: bit0 = first block is not a panel start, bit1 = empty panels inside
 // per chunk: bit0 = first block is not a panel start, bit1 = empty panels
-// inside, bit2 = lane-per-panel mode (>= kLppMinPanels whole, non-empty panels
+// inside, bit2 = lane-per-panel-row mode (>= kLppMinLanes lanes' worth of whole, non-empty panels
 // of similar length: one lane sums a whole panel, no cross-lane reduction)
-constexpr int64_t kLppMinPanels = 12;
-__global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np,
+constexpr int64_t kLppMinLanes = 24;  // panels * r
+__global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                                    const int64_t *__restrict__ chunk_b,
                                    const int64_t *__restrict__ chunk_p,
                                    const int64_t *__restrict__ rowptr,
@@ -243,7 +243,7 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np,
         const int64_t cb0 = chunk_b[c], cb1 = chunk_b[c + 1];
         const bool ends_clean = hi_p >= np ? cb1 == nb : rowptr[hi_p] == cb1;
         const int64_t npc = hi_p - lo_p;
-        if (ends_clean && npc >= kLppMinPanels) {
+        if (ends_clean && npc * r >= kLppMinLanes) {
             int64_t maxlen = 0;
             for (int64_t p = lo_p; p < hi_p; ++p) maxlen = max(maxlen, rowptr[p + 1] - rowptr[p]);
             if (maxlen <= 64 && maxlen * npc <= 2 * (cb1 - cb0) + 4 * npc) f |= 4;
@@ -550,8 +550,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         SPC5_TRY(build_chunks(m, cb, st));
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
-            P.num_chunks, nb, np, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels, P.num_empty,
-            P.chunk_flags);
+            P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
+            P.num_empty, P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
         unsigned long long *d_st = nullptr, h_st[3] = {0, 0, 0};
         SPC5_TRY(dev_alloc(&d_st, 3));

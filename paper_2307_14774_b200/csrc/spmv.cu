@@ -340,11 +340,35 @@ __device__ __forceinline__ int64_t lds_s64(uint32_t addr) {
     return v;
 }
 
-// Lane-per-panel mode (chunk flag bit2): lane q owns panel p0+q of the chunk
-// and walks its blocks in order, so a panel is summed by one lane with no
-// cross-lane reduction, and lanes of one step touch consecutive panels
-// (neighbouring x for banded matrices).  Value offsets: per-lane counts and
-// one warp scan per 32 panels.
+// popcount of the masks of rows 0..rr-1 of a lane's block (rr at run time)
+template <int LB, int MB>
+__device__ __forceinline__ int popc_below(const LaneMasks<LB> &mk, int rr) {
+    const int bits = rr * 8 * MB;  // bit offset of row rr in the packed masks
+    int c = 0;
+#pragma unroll
+    for (int i = 0; i < LaneMasks<LB>::N; ++i) {
+        const int lo = i * 32;
+        const uint32_t keep = bits >= lo + 32 ? 0xffffffffu
+                                              : (bits <= lo ? 0u : ((1u << (bits - lo)) - 1u));
+        c += __popc(mk.w[i] & keep);
+    }
+    return c;
+}
+template <int LB, int MB>
+__device__ __forceinline__ uint32_t row_rt(const LaneMasks<LB> &mk, int rr) {
+    const int bit = rr * 8 * MB;
+    constexpr uint32_t M = MB == 1 ? 0xffu : 0xffffu;
+    uint32_t w = mk.w[0];
+#pragma unroll
+    for (int i = 1; i < LaneMasks<LB>::N; ++i) w = (bit >> 5) == i ? mk.w[i] : w;
+    return (w >> (bit & 31)) & M;
+}
+
+// Lane-per-panel-row mode (chunk flag bit2): the R lanes of a group own the R
+// rows of panel p0+q and walk the panel's blocks in order, so each row is
+// summed by one lane with no cross-lane reduction, and the 32/R groups of a
+// step touch consecutive panels (neighbouring x for banded matrices).  Value
+// offsets: per-panel counts and one warp scan per 32/R panels.
 template <typename T, typename MT, int R, bool GENERIC>
 __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t p0, int npc,
                                           uint32_t a_rp, uint32_t a_col, uint32_t a_mask,
@@ -352,70 +376,62 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t
                                           T *__restrict__ y) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;
+    constexpr int PP = 32 / R;  // panels per step
+    const int rr = lane % R;
+    const int grp = lane / R;
     uint32_t vbase = 0;
-    for (int q0 = 0; q0 < npc; q0 += 32) {
-        const int q = q0 + lane;
+    for (int q0 = 0; q0 < npc; q0 += PP) {
+        const int q = q0 + grp;
         const bool pv = q < npc;
         const uint32_t rq = a_rp + (uint32_t)min(q, npc - 1) * 8u;  // staged rowptr[p0 + q]
         const int64_t s64 = lds_s64(rq), e64 = lds_s64(rq + 8u);
         const int s = (int)(s64 - b0);
         const int len = pv ? (int)(e64 - s64) : 0;
         const int maxlen = __reduce_max_sync(kFull, len);
-        int cnt = 0;
+        int cnt = 0;  // values of the whole panel (same in every lane of the group)
         for (int j = 0; j < maxlen; ++j) {
             LaneMasks<LB> mk;
             mk.load(a_mask + (uint32_t)(j < len ? s + j : 0) * LB);
             cnt += j < len ? mk.popc() : 0;
         }
-        const int incl = warp_incl_scan(cnt);
+        const int incl = warp_incl_scan(rr == 0 ? cnt : 0);
         const int total = __shfl_sync(kFull, incl, 31);
-        uint32_t vaddr = a_val + (vbase + (uint32_t)(incl - cnt)) * (uint32_t)sizeof(T);
+        const int excl = __shfl_sync(kFull, incl - (rr == 0 ? cnt : 0), lane - rr);
+        uint32_t vaddr = a_val + (vbase + (uint32_t)excl) * (uint32_t)sizeof(T);
         vbase += (uint32_t)total;
-        double acc[R];
-#pragma unroll
-        for (int g = 0; g < R; ++g) acc[g] = 0.0;
+        double acc = 0.0;
         // three blocks per step: all their x gathers are in flight before the
         // first FMA (values still accumulate in storage order)
         constexpr int U = 3;
         for (int j = 0; j < maxlen; j += U) {
-            uint32_t col[U], vr[U];
-            LaneMasks<LB> mk[U];
+            uint32_t col[U], vr[U], m[U];
+            int h[U], cm = 0;
+            uint32_t vnext = vaddr;
 #pragma unroll
             for (int k = 0; k < U; ++k) {
                 const bool ok = j + k < len;
                 const uint32_t bk = (uint32_t)(ok ? s + j + k : 0);
                 col[k] = lds_u32(a_col + bk * 4u);
-                mk[k].load(a_mask + bk * LB);
-                mk[k].clear_if(ok);
+                LaneMasks<LB> mk;
+                mk.load(a_mask + bk * LB);
+                mk.clear_if(ok);
+                // block k's values: rows 0..R-1 in order; this lane's row starts
+                // after the rows below it
+                vr[k] = vnext + (uint32_t)popc_below<LB, MB>(mk, rr) * (uint32_t)sizeof(T);
+                vnext += (uint32_t)mk.popc() * (uint32_t)sizeof(T);
+                m[k] = R == 1 ? mk.w[0] : row_rt<LB, MB>(mk, rr);
+                h[k] = __popc(m[k]);
+                cm = max(cm, h[k]);
             }
-            // storage order: block j's rows 0..R-1, then block j+1's, ...
-            vr[0] = vaddr;
-#pragma unroll
-            for (int k = 1; k < U; ++k)
-                vr[k] = vr[k - 1] + (uint32_t)mk[k - 1].popc() * (uint32_t)sizeof(T);
-            vaddr = vr[U - 1] + (uint32_t)mk[U - 1].popc() * (uint32_t)sizeof(T);
-#pragma unroll
-            for (int g = 0; g < R; ++g) {
-                uint32_t m[U];
-                int h[U], cm = 0;
-#pragma unroll
-                for (int k = 0; k < U; ++k) {
-                    m[k] = mk[k].template row<MB>(g);
-                    h[k] = __popc(m[k]);
-                    cm = max(cm, h[k]);
-                }
-                uint32_t vg[U];
-#pragma unroll
-                for (int k = 0; k < U; ++k) vg[k] = vr[k];
-                row_dispatch<T, U>(acc[g], m, h, x, col, vg, __reduce_max_sync(kFull, cm));
-#pragma unroll
-                for (int k = 0; k < U; ++k)
-                    vr[k] += (uint32_t)__popc(mk[k].template row<MB>(g)) * (uint32_t)sizeof(T);
-            }
+            vaddr = vnext;
+            row_dispatch<T, U>(acc, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
         }
         const int64_t p = p0 + q;
-        if (pv && (!GENERIC || (p >= a.p_lo && p < a.p_hi)))
-            store_rows<T, R>(y, p * R, a.num_rows, acc, a.accumulate);
+        const int64_t row = p * R + rr;
+        if (pv && row < a.num_rows && (!GENERIC || (p >= a.p_lo && p < a.p_hi))) {
+            const T sv = (T)acc;
+            y[row] = a.accumulate ? y[row] + sv : sv;
+        }
     }
 }
 
