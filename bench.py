@@ -196,14 +196,13 @@ def cpu_product_sample(cfg_id, formats, budget_s=15.0, threads=None):
     per_fmt_budget = budget_s / len(formats)
     for (r, vs) in formats:
         s = oracle.csr_to_spc5(m, r, vs)
-        y = np.zeros(m.num_rows, m.values.dtype)
-        oracle.spmv_spc5_scalar(s, x, y, threads=threads)  # warm-up + parity vector
-        ys[(r, vs)] = y
+        run = oracle.ScalarRunner(s, x, threads)
+        run.run()  # warm-up (page faults, thread pool); also the parity vector
+        ys[(r, vs)] = run.y().copy()
         t_f, reps = 0.0, 0
-        while t_f < per_fmt_budget and reps < 50:
-            yy = np.zeros(m.num_rows, m.values.dtype)
+        while t_f < per_fmt_budget and reps < 200:
             t0 = time.perf_counter()
-            oracle.spmv_spc5_scalar(s, x, yy, threads=threads)
+            run.run()
             t_f += time.perf_counter() - t0
             reps += 1
         flops += 2.0 * m.nnz * reps
@@ -228,11 +227,14 @@ def reference_arm(args, formats):
     threads = oracle.threads()
     mats = {f: oracle.csr_to_spc5(m, *f) for f in formats}
     # one step = a bounded sample: the same fraction of every format's panels
-    y = np.zeros(m.num_rows, m.values.dtype)
+    runners = [oracle.ScalarRunner(mats[f], x, threads) for f in formats]
+    for rn in runners:
+        rn.run()
     t0 = time.perf_counter()
-    for f in formats:
-        oracle.spmv_spc5_scalar(mats[f], x, y, threads=threads)
+    for rn in runners:
+        rn.run()
     full = time.perf_counter() - t0
+    del runners
     frac = min(1.0, 0.25 / max(full, 1e-9))
 
     def sub(s, lo, hi):
@@ -246,15 +248,15 @@ def reference_arm(args, formats):
     for f in formats:
         s = mats[f]
         hi = max(1, int(s.num_panels * frac))
-        samples.append(sub(s, 0, hi))
-    nnz_step = sum(sm.nnz for sm in samples)
+        samples.append(oracle.ScalarRunner(sub(s, 0, hi), x, threads))
+    nnz_step = sum(sm.s.nnz for sm in samples)
     for _ in range(args.warmup):
         for sm in samples:
-            oracle.spmv_spc5_scalar(sm, x, np.zeros(sm.num_rows, m.values.dtype), threads=threads)
+            sm.run()
     t0 = time.perf_counter()
     for _ in range(args.steps):
         for sm in samples:
-            oracle.spmv_spc5_scalar(sm, x, np.zeros(sm.num_rows, m.values.dtype), threads=threads)
+            sm.run()
     el = time.perf_counter() - t0
     val = 2.0 * nnz_step * args.steps / el / 1e9
     sample = (f"{frac:.3f} of the panels of each of {[fmt_key(*f) for f in formats]} per step "

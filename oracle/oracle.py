@@ -186,6 +186,36 @@ def spmv_spc5_scalar(s, x, y, threads: int = 1) -> None:
     y[:s.num_rows] += ypad[:s.num_rows]
 
 
+class ScalarRunner:
+    """The C scalar kernel bound to one matrix/x, checks done once (CPU-baseline timing).
+
+    run() is exactly oracle_spmv_scalar_* over all panels (kernels.py:121-143)
+    into a preallocated ypad; it returns the value cursor.
+    """
+
+    def __init__(self, s, x, threads: int = 1):
+        self.s = s
+        dt = s.values.dtype
+        self.x = np.ascontiguousarray(np.asarray(x, dtype=dt))
+        self.rp = np.ascontiguousarray(s.block_rowptr, dtype=np.int64)
+        self.ci = np.ascontiguousarray(s.block_colidx)
+        self.mk = np.ascontiguousarray(s.block_masks)
+        self.va = np.ascontiguousarray(s.values)
+        self.ypad = np.zeros(s.num_panels * s.r, dtype=dt)
+        self.threads = int(threads)
+        self.fn = lib().oracle_spmv_scalar_f64 if dt == np.float64 else lib().oracle_spmv_scalar_f32
+        if block_value_offsets(s)[-1] != s.nnz:
+            raise RuntimeError("value cursor mismatch")
+
+    def run(self) -> int:
+        self.ypad[:] = 0
+        return int(self.fn(self.s.num_panels, self.s.r, self.s.vs, _p(self.rp), _p(self.ci),
+                           _p(self.mk), _p(self.va), _p(self.x), _p(self.ypad), self.threads))
+
+    def y(self):
+        return self.ypad[:self.s.num_rows]
+
+
 def partition_by_nnz(s, workers: int) -> list[tuple[int, int]]:
     """parallel.py:31-52 restated; returns the list of (lo, hi) panel ranges."""
     if workers < 1:
