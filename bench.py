@@ -348,14 +348,19 @@ def ours_single(args, formats):
                              "nnz": mats[f].nnz, "num_blocks": mats[f].num_blocks,
                              "max_scaled_err": validation[fmt_key(*f)][0]}
     achieved = tot_bytes / tot_time / 1e9
-    traffic = None
+    # traffic: DRAM bytes per K2 launch from the committed ncu --set full capture
+    # (mean over the format launches, like alg_bytes_per_launch below)
+    traffic, traffic_fmt = None, None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
         tr = json.loads(tf.read_text()).get(f"config{args.config}")
-        if tr:
-            traffic = tr
+        if tr and tr.get("per_launch_bytes"):
+            traffic_fmt = tr["per_launch_bytes"]
+            traffic = sum(traffic_fmt.values()) / len(traffic_fmt)
     roofline = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s",
                 "frac": achieved / peak, "traffic": traffic,
+                "alg_bytes_per_launch": tot_bytes / len(formats),
+                "traffic_per_launch_by_kernel": traffic_fmt,
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                 if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
                 "alg_bytes_per_step": tot_bytes,

@@ -570,7 +570,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.chunk_target = cb;
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
         const int64_t mb = P.max_chunk_blocks;
-        P.lay_rp = a16((mb / 32 + 2) * 4 + 32);
+        P.lay_rp = 64 + a16((mb / 32 + 2) * 4 + 32);  // 64-byte chunk header, then bits
         P.lay_col = P.lay_rp + (P.max_lpp_panels ? a16((P.max_lpp_panels + 1) * 8 + 32) : 0);
         P.lay_mask = P.lay_col + a16(mb * 4 + 32);
         P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);

@@ -58,7 +58,8 @@ struct SpmvArgs {
 };
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kSlots = 2;  // chunks in flight per warp
+constexpr int kSlots = 2;    // chunks in flight per warp
+constexpr uint32_t kHdr = 64;  // slot header bytes (chunk descriptor)
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -326,8 +327,15 @@ __device__ __forceinline__ void issue_chunk(const SpmvArgs &a, const ChunkDesc &
         r0 = (uint64_t)(a.rowptr + d.p0);
         br = (uint32_t)(align_up16((uint64_t)(a.rowptr + d.pe + 1)) - align_dn16(r0));
     }
+    // slot header for the consumer: b0, b1, v0, p0, pe, flags
+    asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(slot), "l"(d.b0), "l"(d.b1) : "memory");
+    asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(slot + 16), "l"(d.v0), "l"(d.p0)
+                 : "memory");
+    asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(slot + 32), "l"(d.pe),
+                 "l"((int64_t)d.flags)
+                 : "memory");
     mbar_expect_tx(bar, bw + br + bc + bm + bv);
-    bulk_g2s(slot, (const void *)align_dn16(w0), bw, bar, pol);
+    bulk_g2s(slot + kHdr, (const void *)align_dn16(w0), bw, bar, pol);
     if (br) bulk_g2s(slot + a.lay_rp, (const void *)align_dn16(r0), br, bar, pol);
     bulk_g2s(slot + a.lay_col, (const void *)align_dn16(c0), bc, bar, pol);
     bulk_g2s(slot + a.lay_mask, (const void *)align_dn16(m0), bm, bar, pol);
@@ -474,17 +482,16 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
     const int wpc = blockDim.x >> 5;  // warps per CTA
     const int64_t stride = (int64_t)gridDim.x * wpc;
     const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * wpc + warp;
-    // descriptors of chunks k, k+1, k+2 (fields spread over lanes 0..6)
-    int64_t dq0 = desc_load(a, cfirst, cfirst < a.c_hi, lane);
-    int64_t dq1 = desc_load(a, cfirst + stride, cfirst + stride < a.c_hi, lane);
-    int64_t dq2 = desc_load(a, cfirst + 2 * stride, cfirst + 2 * stride < a.c_hi, lane);
+    // prologue: fill the ring with the warp's first two chunks
     {
+        const int64_t d0 = desc_load(a, cfirst, cfirst < a.c_hi, lane);
+        const int64_t d1 = desc_load(a, cfirst + stride, cfirst + stride < a.c_hi, lane);
         if (cfirst < a.c_hi) {
-            const ChunkDesc d = desc_get(dq0);
+            const ChunkDesc d = desc_get(d0);
             if (lane == 0) issue_chunk<T, LB>(a, d, ring, bars, pol);
         }
         if (cfirst + stride < a.c_hi) {
-            const ChunkDesc d = desc_get(dq1);
+            const ChunkDesc d = desc_get(d1);
             if (lane == 0) issue_chunk<T, LB>(a, d, ring + a.lay_bytes, bars + 1, pol);
         }
     }
@@ -493,9 +500,16 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
     for (int64_t c = cfirst; c < a.c_hi; c += stride, ++it) {
         const int slot_i = it % kSlots;
         const uint32_t parity = (it / kSlots) & 1u;
-        const ChunkDesc dd = desc_get(dq0);
-        const int64_t b0 = dd.b0, b1 = dd.b1, v0 = dd.v0, p0 = dd.p0, pe = dd.pe;
-        const int flags = dd.flags;
+        // descriptor of the chunk this slot is refilled with at the end of the
+        // iteration: loaded now, its latency hides behind this chunk's work
+        const int64_t dnext = desc_load(a, c + 2 * stride, c + 2 * stride < a.c_hi, lane);
+        const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
+        mbar_wait(bars + slot_i, parity);
+        // this chunk's descriptor, written into the slot header by the producer
+        const int64_t b0 = lds_s64(sbase), b1 = lds_s64(sbase + 8);
+        const int64_t v0 = lds_s64(sbase + 16), p0 = lds_s64(sbase + 24);
+        const int64_t pe = lds_s64(sbase + 32);
+        const int flags = (int)lds_s64(sbase + 40);
         const bool head_mid = flags & 1;  // first block continues a panel of earlier chunks
         const bool slow = flags & 2;      // empty panels inside: search block_rowptr
         const int n = (int)(b1 - b0);
@@ -504,9 +518,8 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
             a0 = (int)(max(b0, a.b_lo) - b0);
             a1 = (int)(min(b1, a.b_hi) - b0);
         }
-        const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
         // arrays are 256-byte aligned: a region's offset in its slot is its start mod 16
-        const uint32_t a_bits = sbase + (uint32_t)((((b0 + a.off32) >> 5) * 4) & 15);
+        const uint32_t a_bits = sbase + kHdr + (uint32_t)((((b0 + a.off32) >> 5) * 4) & 15);
         const uint32_t a_rp = sbase + a.lay_rp + (uint32_t)((p0 * 8) & 15);
         const uint32_t a_col = sbase + a.lay_col + (uint32_t)((b0 * 4) & 15);
         const uint32_t a_mask = sbase + a.lay_mask + (uint32_t)((b0 * LB) & 15);
@@ -518,8 +531,6 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
         int carry_panel = 0;           // relative to p0
         int pcur = head_mid ? 0 : -1;  // panel (rel. p0) of the block before the window
         uint32_t vrel = 0;
-
-        mbar_wait(bars + slot_i, parity);
 
         if (flags & 4) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, b0, p0, (int)(pe - p0), a_rp, a_col, a_mask, a_val,
@@ -632,15 +643,12 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
         __syncwarp();
         const int64_t cn = c + 2 * stride;
         if (cn < a.c_hi) {
-            const ChunkDesc d2 = desc_get(dq2);
+            const ChunkDesc d2 = desc_get(dnext);
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 issue_chunk<T, LB>(a, d2, sbase, bars + slot_i, pol);
             }
         }
-        dq0 = dq1;
-        dq1 = dq2;
-        dq2 = desc_load(a, c + 3 * stride, c + 3 * stride < a.c_hi, lane);
     }
 }
 
