@@ -38,11 +38,14 @@ struct Plan {
     int64_t split_len = 256;        // long panels are cut at global multiples of this
     int64_t max_chunk_blocks = 0, max_chunk_values = 0;
     int64_t max_lpp_panels = 0;     // panels of the largest lane-per-panel chunk
-    int64_t lay_rp = 0, lay_col = 0, lay_mask = 0, lay_val = 0;  // slot: bits|rp|col|mask|val
+    int64_t lay_rp = 0, lay_col = 0, lay_mask = 0, lay_val = 0;  // slot: hdr|bits|rec|col|mask|val
     int slot_bytes = 0;
     int64_t num_granules = 0;
     uint32_t *pstart_bits = nullptr;  // [num_granules] bit i of word g: block 32g-off32+i starts a panel
     uint8_t *chunk_flags = nullptr;   // [num_chunks] bit0: starts inside a panel, bit1: has empty panels
+    // lane-per-panel chunks: record of panel p (chunk c) at p + c: first block
+    // (bits 0-15) and first value (bits 16-31) relative to the chunk start
+    uint32_t *lpr_rec = nullptr;      // [num_panels + num_chunks + 2]
 };
 
 struct Matrix {

@@ -19,6 +19,7 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <cstdlib>
 #include <algorithm>
 #include <string>
 #include <vector>
@@ -217,11 +218,12 @@ __global__ void pstart_bits_kernel(int64_t np, const int64_t *__restrict__ rowpt
     atomicOr(bits + ((b + off32) >> 5), 1u << ((b + off32) & 31));
 }
 
-// per chunk: bit0 = first block is not a panel start, bit1 = empty panels inside
 // per chunk: bit0 = first block is not a panel start, bit1 = empty panels
-// inside, bit2 = lane-per-panel-row mode (>= kLppMinLanes lanes' worth of whole, non-empty panels
-// of similar length: one lane sums a whole panel, no cross-lane reduction)
-constexpr int64_t kLppMinLanes = 24;  // panels * r
+// inside, bit2 = lane-per-panel-row mode (whole, non-empty panels of similar
+// length, >= kLppMinLanes lanes busy), bits3-4 = log2 G: in that mode each
+// panel row is split over G lanes (contiguous block ranges, partial sums
+// combined by a butterfly), so short chunks still fill the warp
+constexpr int64_t kLppMinLanes = 24;  // panels * r * G
 __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                                    const int64_t *__restrict__ chunk_b,
                                    const int64_t *__restrict__ chunk_p,
@@ -243,16 +245,53 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
         const int64_t cb0 = chunk_b[c], cb1 = chunk_b[c + 1];
         const bool ends_clean = hi_p >= np ? cb1 == nb : rowptr[hi_p] == cb1;
         const int64_t npc = hi_p - lo_p;
-        if (ends_clean && npc * r >= kLppMinLanes) {
+        if (ends_clean && npc > 0 && npc * r <= 32 * 64) {
             int64_t maxlen = 0;
             for (int64_t p = lo_p; p < hi_p; ++p) maxlen = max(maxlen, rowptr[p + 1] - rowptr[p]);
-            if (maxlen <= 64 && maxlen * npc <= 2 * (cb1 - cb0) + 4 * npc) f |= 4;
+            int lg = 0;  // G = 1 << lg lanes per panel row, each with >= 1 block
+            while (lg < 3 && npc * r * (2 << lg) <= 32 && maxlen >= (2 << lg)) ++lg;
+            if (npc * r * (1 << lg) >= kLppMinLanes && maxlen <= 64 * (1 << lg) &&
+                maxlen * npc <= 2 * (cb1 - cb0) + 4 * npc)
+                f |= 4 | (lg << 3);
         }
     }
     flags[c] = f;
 }
 
-// largest panel count of a lane-per-panel chunk (sizes the staged rowptr)
+// panel records of lane-per-panel chunks (warp per chunk): for q = 0..npc,
+// rec[p0 + q + c] = (rowptr[p0+q] - b0) | (values before panel p0+q in the chunk) << 16
+__global__ void lpr_rec_kernel(int64_t nc, int r, int vs, const int64_t *__restrict__ chunk_b,
+                               const int64_t *__restrict__ chunk_p,
+                               const uint8_t *__restrict__ flags, const int64_t *__restrict__ rowptr,
+                               const void *__restrict__ masks, uint32_t *rec) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nc; c += nwarps) {
+        if (!(flags[c] & 4)) continue;
+        const int64_t b0 = chunk_b[c], p0 = chunk_p[c];
+        const int64_t npc = chunk_p[c + 1] - p0;
+        uint32_t running = 0;
+        for (int64_t q0 = 0; q0 <= npc; q0 += 32) {
+            const int64_t q = q0 + lane;
+            const int64_t s = q <= npc ? rowptr[p0 + q] - b0 : 0;
+            int cnt = 0;
+            if (q < npc)
+                for (int64_t b = rowptr[p0 + q]; b < rowptr[p0 + q + 1]; ++b)
+                    for (int rr = 0; rr < r; ++rr) cnt += __popc(load_mask(masks, b * r + rr, vs));
+            int incl = cnt;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int t = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += t;
+            }
+            if (q <= npc)
+                rec[p0 + q + c] = (uint32_t)s | ((running + (uint32_t)(incl - cnt)) << 16);
+            running += (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
+        }
+    }
+}
+
+// largest panel count of a lane-per-panel chunk (sizes the staged records)
 __global__ void lpp_panels_kernel(int64_t nc, const int64_t *__restrict__ chunk_p,
                                   const uint8_t *__restrict__ flags, unsigned long long *out) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -360,6 +399,7 @@ void free_plan(Plan &p) {
     dev_free(p.tile_prefix);
     dev_free(p.pstart_bits);
     dev_free(p.chunk_flags);
+    dev_free(p.lpr_rec);
     delete[] p.h_chunk_b;
     p = Plan{};
 }
@@ -546,6 +586,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         while (sl > 1 && sl * max_block_bytes > 6 * 1024) sl >>= 1;
         P.split_len = sl;
     }
+    int64_t slot_cap = 10 * 1024;  // target ring-slot size (tuning knob SPC5_SLOT_KB)
+    if (const char *e = getenv("SPC5_SLOT_KB")) slot_cap = std::max(1, atoi(e)) * 1024;
     for (int64_t cb = 512;; cb >>= 1) {
         SPC5_TRY(build_chunks(m, cb, st));
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
@@ -571,12 +613,12 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
         const int64_t mb = P.max_chunk_blocks;
         P.lay_rp = 64 + a16((mb / 32 + 2) * 4 + 32);  // 64-byte chunk header, then bits
-        P.lay_col = P.lay_rp + (P.max_lpp_panels ? a16((P.max_lpp_panels + 1) * 8 + 32) : 0);
+        P.lay_col = P.lay_rp + (P.max_lpp_panels ? a16((P.max_lpp_panels + 1) * 4 + 32) : 0);
         P.lay_mask = P.lay_col + a16(mb * 4 + 32);
         P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
                              128 * 128);
-        if (P.slot_bytes <= 10 * 1024 || cb == 1) break;
+        if (P.slot_bytes <= slot_cap || cb == 1) break;
         if (cb <= 32 && P.slot_bytes <= 14 * 1024) break;
         free_chunks(P);
         dev_free(P.chunk_flags);
@@ -584,6 +626,14 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     }
     if (P.slot_bytes > 14 * 1024)
         return fail(SPC5_EINVAL, "a chunk of this matrix does not fit the shared-memory ring");
+    // panel records of the lane-per-panel chunks
+    if (P.max_lpp_panels) {
+        SPC5_TRY(dev_alloc(&P.lpr_rec, (size_t)(np + P.num_chunks + 2)));
+        lpr_rec_kernel<<<(unsigned)std::min<int64_t>(cdiv(P.num_chunks, 8), 65535), 256, 0, st>>>(
+            P.num_chunks, m.r, m.vs, P.chunk_b, P.chunk_p, P.chunk_flags, m.rowptr, m.masks,
+            P.lpr_rec);
+        SPC5_CUDA(cudaGetLastError());
+    }
     // panel-start bitmap
     const int off32 = (int)(((m.block_base % 32) + 32) % 32);
     const int64_t ng = cdiv(nb + off32, 32);

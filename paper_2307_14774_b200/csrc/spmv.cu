@@ -16,7 +16,7 @@
 //    the "value cursor" of kernels.py:211-212 in parallel form.
 //  * panel membership: one bit per block from the plan's panel-start bitmap
 //    (a popcount gives the panel of every lane); chunks holding empty panels
-//    search block_rowptr instead (generic pass).
+//    search block_rowptr instead.
 //  * products: each panel row's set bits, highest first (bfind), x gathered
 //    through the read-only path (x is the only re-read array and stays L2
 //    resident; the matrix stream is loaded evict-first), fp64 accumulation
@@ -28,6 +28,7 @@
 //    summed in an order fixed by global block positions only, so results are
 //    bitwise reproducible across runs, spmv_parallel ranges and GPU shards.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -55,11 +56,13 @@ struct SpmvArgs {
     int accumulate;
     uint32_t lay_rp, lay_col, lay_mask, lay_val, lay_bytes;  // slot layout (bytes)
     int max_rp;        // panel ends staged for lane-per-panel chunks
+    const uint32_t *lpr_rec;  // lane-per-panel chunks: per panel (block, value) offsets
 };
 
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kSlots = 2;    // chunks in flight per warp
 constexpr uint32_t kHdr = 64;  // slot header bytes (chunk descriptor)
+constexpr uint32_t kRingOff = 128;  // barriers before the ring
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -176,6 +179,39 @@ __device__ __forceinline__ float lds_pred<float>(uint32_t addr, bool pred) {
     return v;
 }
 
+template <typename T>
+__device__ __forceinline__ T lds_val(uint32_t addr);
+template <>
+__device__ __forceinline__ double lds_val<double>(uint32_t addr) {
+    double v;
+    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
+    return v;
+}
+template <>
+__device__ __forceinline__ float lds_val<float>(uint32_t addr) {
+    float v;
+    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
+    return v;
+}
+
+// acc += v * x for an occupied slot (u < h): fused for f64; for f32 the
+// product is rounded in f32 (as the reference forms it), accumulated in f64
+template <typename T>
+__device__ __forceinline__ void slot_mac(double &acc, T vv, T xv, int u, int h);
+template <>
+__device__ __forceinline__ void slot_mac<double>(double &acc, double vv, double xv, int u, int h) {
+    asm("{\n .reg .pred q;\n setp.lt.s32 q, %1, %2;\n @q fma.rn.f64 %0, %3, %4, %0;\n}"
+        : "+d"(acc)
+        : "r"(u), "r"(h), "d"(vv), "d"(xv));
+}
+template <>
+__device__ __forceinline__ void slot_mac<float>(double &acc, float vv, float xv, int u, int h) {
+    asm("{\n .reg .pred q;\n .reg .f32 t;\n .reg .f64 d;\n setp.lt.s32 q, %1, %2;\n"
+        " mul.rn.f32 t, %3, %4;\n cvt.f64.f32 d, t;\n @q add.rn.f64 %0, %0, d;\n}"
+        : "+d"(acc)
+        : "r"(u), "r"(h), "f"(vv), "f"(xv));
+}
+
 // acc += v * x: fused for f64; for f32 the product is rounded in f32 (as the
 // reference forms it) and accumulated in f64.  Empty slots add exact zeros.
 template <typename T>
@@ -231,22 +267,32 @@ __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h
                                           const T *__restrict__ x, const uint32_t (&col)[U],
                                           const uint32_t (&vaddr)[U]) {
     T vv[U][NS], xv[U][NS];
+    uint32_t vtop[U];  // value of the block's highest remaining bit; slot u reads vtop - u
+    int h0[U];
+    const T *xb[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        h0[k] = h[k];
+        vtop[k] = vaddr[k] + (uint32_t)(h[k] - 1) * (uint32_t)sizeof(T);
+        h[k] = max(h[k] - NS, 0);  // >= 0 keeps empty slots' loads inside the slot
+        xb[k] = x + col[k];
+    }
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
 #pragma unroll
         for (int k = 0; k < U; ++k) {
-            const bool ok = m[k] != 0u;
             const uint32_t pos = bfind(m[k]);
             m[k] &= ~(1u << pos);
-            --h[k];
-            xv[k][u] = ldg_pred(x + (col[k] + pos), ok);
-            vv[k][u] = lds_pred<T>(vaddr[k] + (uint32_t)h[k] * (uint32_t)sizeof(T), ok);
+            xv[k][u] = ldg_pred(xb[k] + pos, u < h0[k]);
+            // an empty slot's value load stays inside the slot (the masks
+            // precede the values); its product is skipped
+            vv[k][u] = lds_val<T>(vtop[k] - (uint32_t)(u * sizeof(T)));
         }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
 #pragma unroll
-        for (int u = 0; u < NS; ++u) mac<T>(acc, vv[k][u], xv[k][u]);
+        for (int u = 0; u < NS; ++u) slot_mac<T>(acc, vv[k][u], xv[k][u], u, h0[k]);
     }
 }
 
@@ -304,12 +350,12 @@ __device__ __forceinline__ ChunkDesc desc_get(int64_t d) {
     return r;
 }
 
-// Lane 0 of the warp: copy one chunk (panel-start words, [panel ends for
+// Lane 0 of the warp: copy one chunk (panel-start words, [panel records for
 // lane-per-panel chunks], column starts, masks, values) into the slot at
 // shared address `slot` with bulk copies that complete on one mbarrier.
 template <typename T, int LB>
-__device__ __forceinline__ void issue_chunk(const SpmvArgs &a, const ChunkDesc &d, uint32_t slot,
-                                            uint64_t *bar, uint64_t pol) {
+__device__ __forceinline__ void issue_chunk(const SpmvArgs &a, const ChunkDesc &d, int64_t c,
+                                            uint32_t slot, uint64_t *bar, uint64_t pol) {
     const uint64_t w0 = (uint64_t)(a.pstart_bits + ((d.b0 + a.off32) >> 5));
     const uint64_t w1 = (uint64_t)(a.pstart_bits + ((d.b1 - 1 + a.off32) >> 5) + 1);
     const uint64_t c0 = (uint64_t)(a.colidx + d.b0), c1 = (uint64_t)(a.colidx + d.b1);
@@ -323,9 +369,9 @@ __device__ __forceinline__ void issue_chunk(const SpmvArgs &a, const ChunkDesc &
     const uint32_t bv = d.v1 > d.v0 ? (uint32_t)(align_up16(q1) - align_dn16(q0)) : 0u;
     uint32_t br = 0;
     uint64_t r0 = 0;
-    if (d.flags & 4) {  // panel ends rowptr[p0 .. pe]
-        r0 = (uint64_t)(a.rowptr + d.p0);
-        br = (uint32_t)(align_up16((uint64_t)(a.rowptr + d.pe + 1)) - align_dn16(r0));
+    if (d.flags & 4) {  // panel records p0 .. pe (stored at p0 + c)
+        r0 = (uint64_t)(a.lpr_rec + d.p0 + c);
+        br = (uint32_t)(align_up16((uint64_t)(a.lpr_rec + d.pe + c + 1)) - align_dn16(r0));
     }
     // slot header for the consumer: b0, b1, v0, p0, pe, flags
     asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(slot), "l"(d.b0), "l"(d.b1) : "memory");
@@ -372,52 +418,70 @@ __device__ __forceinline__ uint32_t row_rt(const LaneMasks<LB> &mk, int rr) {
     return (w >> (bit & 31)) & M;
 }
 
-// Lane-per-panel-row mode (chunk flag bit2): the R lanes of a group own the R
-// rows of panel p0+q and walk the panel's blocks in order, so each row is
-// summed by one lane with no cross-lane reduction, and the 32/R groups of a
-// step touch consecutive panels (neighbouring x for banded matrices).  Value
-// offsets: per-panel counts and one warp scan per 32/R panels.
+// Lane-per-panel-row mode (chunk flag bit2): the R*G lanes of a group own
+// panel p0+q; lane (rr, sub) sums row rr over the sub-th of G contiguous
+// block ranges of the panel, in storage order, and the G partial sums of a
+// row meet in a butterfly (G = 1 << lg, chunk flag bits 3-4).  The 32/(R*G)
+// groups of a step touch consecutive panels (neighbouring x for banded
+// matrices).  The plan's panel records give each panel's first block and
+// first value inside the chunk (16 bits each), so a lane starts at once;
+// with G > 1 the lanes of a row also count their sub-ranges' values.
+#ifndef SPC5_LPP_U
+#define SPC5_LPP_U 3
+#endif
 template <typename T, typename MT, int R, bool GENERIC>
-__device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t p0, int npc,
-                                          uint32_t a_rp, uint32_t a_col, uint32_t a_mask,
+__device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t p0, int npc, int lg,
+                                          uint32_t a_rec, uint32_t a_col, uint32_t a_mask,
                                           uint32_t a_val, int lane, const T *__restrict__ x,
                                           T *__restrict__ y) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;
-    constexpr int PP = 32 / R;  // panels per step
-    const int rr = lane % R;
-    const int grp = lane / R;
-    uint32_t vbase = 0;
+    constexpr int LGR = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
+    const int G = 1 << lg;
+    const int sub = lane & (G - 1);
+    const int rr = (lane >> lg) & (R - 1);
+    const int grp = lane >> (lg + LGR);
+    const int PP = 32 >> (lg + LGR);  // panels per step
     for (int q0 = 0; q0 < npc; q0 += PP) {
         const int q = q0 + grp;
         const bool pv = q < npc;
-        const uint32_t rq = a_rp + (uint32_t)min(q, npc - 1) * 8u;  // staged rowptr[p0 + q]
-        const int64_t s64 = lds_s64(rq), e64 = lds_s64(rq + 8u);
-        const int s = (int)(s64 - b0);
-        const int len = pv ? (int)(e64 - s64) : 0;
-        const int maxlen = __reduce_max_sync(kFull, len);
-        int cnt = 0;  // values of the whole panel (same in every lane of the group)
-        for (int j = 0; j < maxlen; ++j) {
-            LaneMasks<LB> mk;
-            mk.load(a_mask + (uint32_t)(j < len ? s + j : 0) * LB);
-            cnt += j < len ? mk.popc() : 0;
+        const uint32_t rq = a_rec + (uint32_t)min(q, npc - 1) * 4u;
+        const uint32_t r0 = lds_u32(rq), r1 = lds_u32(rq + 4u);
+        const int s0 = (int)(r0 & 0xffffu);
+        const int len = pv ? (int)(r1 & 0xffffu) - s0 : 0;
+        int s = s0, my = len;
+        uint32_t vofs = r0 >> 16;
+        if (G > 1) {  // sub-range of the panel and the values before it
+            const int per = (len + G - 1) >> lg;
+            const int lo = min(sub * per, len);
+            my = min(lo + per, len) - lo;
+            s = s0 + lo;
+            int cnt = 0;  // values of this lane's range (all R rows)
+            for (int j = 0; j < my; ++j) {
+                LaneMasks<LB> mk;
+                mk.load(a_mask + (uint32_t)(s + j) * LB);
+                cnt += mk.popc();
+            }
+            int incl = cnt;  // inclusive scan over the G lanes of the row
+            for (int d = 1; d < G; d <<= 1) {
+                const int t = __shfl_up_sync(kFull, incl, d);
+                if (sub >= d) incl += t;
+            }
+            vofs += (uint32_t)(incl - cnt);
         }
-        const int incl = warp_incl_scan(rr == 0 ? cnt : 0);
-        const int total = __shfl_sync(kFull, incl, 31);
-        const int excl = __shfl_sync(kFull, incl - (rr == 0 ? cnt : 0), lane - rr);
-        uint32_t vaddr = a_val + (vbase + (uint32_t)excl) * (uint32_t)sizeof(T);
-        vbase += (uint32_t)total;
+        const int maxlen = __reduce_max_sync(kFull, my);
+        uint32_t vaddr = a_val + vofs * (uint32_t)sizeof(T);
         double acc = 0.0;
-        // three blocks per step: all their x gathers are in flight before the
+        // U blocks per step: all their x gathers are in flight before the
         // first FMA (values still accumulate in storage order)
-        constexpr int U = 3;
+        constexpr int U = SPC5_LPP_U;
         for (int j = 0; j < maxlen; j += U) {
             uint32_t col[U], vr[U], m[U];
             int h[U], cm = 0;
             uint32_t vnext = vaddr;
 #pragma unroll
             for (int k = 0; k < U; ++k) {
-                const bool ok = j + k < len;
+                const bool ok = j + k < my;
                 const uint32_t bk = (uint32_t)(ok ? s + j + k : 0);
                 col[k] = lds_u32(a_col + bk * 4u);
                 LaneMasks<LB> mk;
@@ -434,9 +498,10 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t
             vaddr = vnext;
             row_dispatch<T, U>(acc, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
         }
+        for (int o = 1; o < G; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
         const int64_t p = p0 + q;
         const int64_t row = p * R + rr;
-        if (pv && row < a.num_rows && (!GENERIC || (p >= a.p_lo && p < a.p_hi))) {
+        if (sub == 0 && pv && row < a.num_rows && (!GENERIC || (p >= a.p_lo && p < a.p_hi))) {
             const T sv = (T)acc;
             y[row] = a.accumulate ? y[row] + sv : sv;
         }
@@ -448,7 +513,10 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t b0, int64_t
 // GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
 // spmv_parallel); the arithmetic per panel is identical.
 template <typename T, typename MT, int R, bool GENERIC>
-__global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
+#ifndef SPC5_K2_MINB
+#define SPC5_K2_MINB 2
+#endif
+__global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs a) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;  // mask bytes per lane (<= 16)
     extern __shared__ __align__(128) uint8_t smem[];
@@ -459,7 +527,7 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
     T *__restrict__ y = static_cast<T *>(a.y);
 
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * kSlots;
-    const uint32_t ring = smem_addr(smem) + 128 + (uint32_t)(warp * kSlots) * a.lay_bytes;
+    const uint32_t ring = smem_addr(smem) + kRingOff + (uint32_t)(warp * kSlots) * a.lay_bytes;
     if (lane == 0) {
 #pragma unroll
         for (int i = 0; i < kSlots; ++i) mbar_init(bars + i, 1);
@@ -482,27 +550,28 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
     const int wpc = blockDim.x >> 5;  // warps per CTA
     const int64_t stride = (int64_t)gridDim.x * wpc;
     const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * wpc + warp;
+    const int64_t c_end = a.c_hi;
     // prologue: fill the ring with the warp's first two chunks
     {
-        const int64_t d0 = desc_load(a, cfirst, cfirst < a.c_hi, lane);
-        const int64_t d1 = desc_load(a, cfirst + stride, cfirst + stride < a.c_hi, lane);
-        if (cfirst < a.c_hi) {
+        const int64_t d0 = desc_load(a, cfirst, cfirst < c_end, lane);
+        const int64_t d1 = desc_load(a, cfirst + stride, cfirst + stride < c_end, lane);
+        if (cfirst < c_end) {
             const ChunkDesc d = desc_get(d0);
-            if (lane == 0) issue_chunk<T, LB>(a, d, ring, bars, pol);
+            if (lane == 0) issue_chunk<T, LB>(a, d, cfirst, ring, bars, pol);
         }
-        if (cfirst + stride < a.c_hi) {
+        if (cfirst + stride < c_end) {
             const ChunkDesc d = desc_get(d1);
-            if (lane == 0) issue_chunk<T, LB>(a, d, ring + a.lay_bytes, bars + 1, pol);
+            if (lane == 0) issue_chunk<T, LB>(a, d, cfirst + stride, ring + a.lay_bytes, bars + 1, pol);
         }
     }
 
     uint32_t it = 0;
-    for (int64_t c = cfirst; c < a.c_hi; c += stride, ++it) {
+    for (int64_t c = cfirst; c < c_end; c += stride, ++it) {
         const int slot_i = it % kSlots;
         const uint32_t parity = (it / kSlots) & 1u;
         // descriptor of the chunk this slot is refilled with at the end of the
         // iteration: loaded now, its latency hides behind this chunk's work
-        const int64_t dnext = desc_load(a, c + 2 * stride, c + 2 * stride < a.c_hi, lane);
+        const int64_t dnext = desc_load(a, c + 2 * stride, c + 2 * stride < c_end, lane);
         const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
         mbar_wait(bars + slot_i, parity);
         // this chunk's descriptor, written into the slot header by the producer
@@ -510,6 +579,14 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
         const int64_t v0 = lds_s64(sbase + 16), p0 = lds_s64(sbase + 24);
         const int64_t pe = lds_s64(sbase + 32);
         const int flags = (int)lds_s64(sbase + 40);
+#ifdef SPC5_K2_STREAM_ONLY  // experiment: stream the matrix, skip the products
+        if (b1 >= b0) {
+            if (b1 > b0 + 1000000) y[0] = (T)v0;
+        }
+#else
+        if (false) {}
+#endif
+        else {
         const bool head_mid = flags & 1;  // first block continues a panel of earlier chunks
         const bool slow = flags & 2;      // empty panels inside: search block_rowptr
         const int n = (int)(b1 - b0);
@@ -520,7 +597,7 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
         }
         // arrays are 256-byte aligned: a region's offset in its slot is its start mod 16
         const uint32_t a_bits = sbase + kHdr + (uint32_t)((((b0 + a.off32) >> 5) * 4) & 15);
-        const uint32_t a_rp = sbase + a.lay_rp + (uint32_t)((p0 * 8) & 15);
+        const uint32_t a_rp = sbase + a.lay_rp + (uint32_t)(((p0 + c) * 4) & 15);
         const uint32_t a_col = sbase + a.lay_col + (uint32_t)((b0 * 4) & 15);
         const uint32_t a_mask = sbase + a.lay_mask + (uint32_t)((b0 * LB) & 15);
         const uint32_t a_val = sbase + a.lay_val + (uint32_t)((v0 * (int64_t)sizeof(T)) & 15);
@@ -533,8 +610,8 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
         uint32_t vrel = 0;
 
         if (flags & 4) {  // lane-per-panel chunk
-            lpp_chunk<T, MT, R, GENERIC>(a, b0, p0, (int)(pe - p0), a_rp, a_col, a_mask, a_val,
-                                         lane, x, y);
+            lpp_chunk<T, MT, R, GENERIC>(a, p0, (int)(pe - p0), (flags >> 3) & 3, a_rp, a_col,
+                                         a_mask, a_val, lane, x, y);
         } else
         for (int w = -sh0; w < a1; w += 32) {
             const bool last = w + 32 >= a1;
@@ -639,14 +716,15 @@ __global__ void __launch_bounds__(256, 2) spmv_kernel(const SpmvArgs a) {
             carry_valid = GENERIC ? __shfl_sync(kFull, act, 31) : true;
         }
 
+        }
         // ---- release the slot and refill it with the chunk kSlots ahead
         __syncwarp();
         const int64_t cn = c + 2 * stride;
-        if (cn < a.c_hi) {
+        if (cn < c_end) {
             const ChunkDesc d2 = desc_get(dnext);
             if (lane == 0) {
                 asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_chunk<T, LB>(a, d2, sbase, bars + slot_i, pol);
+                issue_chunk<T, LB>(a, d2, cn, sbase, bars + slot_i, pol);
             }
         }
     }
@@ -684,8 +762,9 @@ template <typename K>
 int launch_ring_kernel(K kernel, const Matrix &m, const SpmvArgs &a, int64_t nslots,
                        cudaStream_t st) {
     // 8 warps per CTA for small slots; 4 for large ones so several CTAs share an SM
-    const int wpc = a.lay_bytes <= 6 * 1024 ? 8 : 4;
-    const size_t smem = 128 + (size_t)wpc * kSlots * a.lay_bytes;  // barriers + ring
+    int wpc = a.lay_bytes <= 6 * 1024 ? 8 : 4;
+    if (const char *e = getenv("SPC5_WPC")) wpc = std::min(8, std::max(1, atoi(e)));  // tuning knob
+    const size_t smem = kRingOff + (size_t)wpc * kSlots * a.lay_bytes;  // barriers + ring
     SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     int per_sm = 0;
@@ -748,6 +827,7 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
     a.chunk_p = P.chunk_p;
     a.chunk_flags = P.chunk_flags;
     a.pstart_bits = P.pstart_bits;
+    a.lpr_rec = P.lpr_rec;
     a.carry = P.carry;
     a.empty_panels = P.empty_panels;
     a.num_empty = P.num_empty;

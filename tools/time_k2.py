@@ -1,0 +1,36 @@
+"""K2 timing only (experiments; no validation): config-2 formats, CUDA events.
+
+usage: python tools/time_k2.py [formats e.g. "1,8;2,8"] [reps]
+"""
+import json
+import sys
+from pathlib import Path
+
+sys.path.insert(0, str(Path(__file__).resolve().parents[1]))
+import torch  # noqa: E402
+
+import bench  # noqa: E402
+from paper_2307_14774_b200 import _native as nat  # noqa: E402
+from paper_2307_14774_b200.blocks import torch_stream  # noqa: E402
+from paper_2307_14774_b200.workloads import x_vector  # noqa: E402
+
+fmts = [tuple(int(v) for v in f.split(",")) for f in
+        (sys.argv[1] if len(sys.argv) > 1 else "1,8;2,8;4,8;8,8").split(";")]
+reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
+mats, nr, nc = bench.build_matrices(2, fmts)
+x = torch.from_numpy(x_vector(nc, "f64")).to("cuda")
+y = torch.empty(nr, dtype=torch.float64, device="cuda")
+out = {}
+for f in fmts:
+    h = mats[f].handle().ptr
+    st = torch_stream()
+    for _ in range(5):
+        nat.check(nat.lib.spc5_spmv(h, x.data_ptr(), y.data_ptr(), 0, st))
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(reps):
+        nat.check(nat.lib.spc5_spmv(h, x.data_ptr(), y.data_ptr(), 0, st))
+    e1.record()
+    torch.cuda.synchronize()
+    out[f"b{f}"] = round(e0.elapsed_time(e1) * 1e3 / reps, 1)
+print(json.dumps(out))
