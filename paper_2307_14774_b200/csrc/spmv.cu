@@ -179,39 +179,6 @@ __device__ __forceinline__ float lds_pred<float>(uint32_t addr, bool pred) {
     return v;
 }
 
-template <typename T>
-__device__ __forceinline__ T lds_val(uint32_t addr);
-template <>
-__device__ __forceinline__ double lds_val<double>(uint32_t addr) {
-    double v;
-    asm("ld.shared.f64 %0, [%1];" : "=d"(v) : "r"(addr));
-    return v;
-}
-template <>
-__device__ __forceinline__ float lds_val<float>(uint32_t addr) {
-    float v;
-    asm("ld.shared.f32 %0, [%1];" : "=f"(v) : "r"(addr));
-    return v;
-}
-
-// acc += v * x for an occupied slot (u < h): fused for f64; for f32 the
-// product is rounded in f32 (as the reference forms it), accumulated in f64
-template <typename T>
-__device__ __forceinline__ void slot_mac(double &acc, T vv, T xv, int u, int h);
-template <>
-__device__ __forceinline__ void slot_mac<double>(double &acc, double vv, double xv, int u, int h) {
-    asm("{\n .reg .pred q;\n setp.lt.s32 q, %1, %2;\n @q fma.rn.f64 %0, %3, %4, %0;\n}"
-        : "+d"(acc)
-        : "r"(u), "r"(h), "d"(vv), "d"(xv));
-}
-template <>
-__device__ __forceinline__ void slot_mac<float>(double &acc, float vv, float xv, int u, int h) {
-    asm("{\n .reg .pred q;\n .reg .f32 t;\n .reg .f64 d;\n setp.lt.s32 q, %1, %2;\n"
-        " mul.rn.f32 t, %3, %4;\n cvt.f64.f32 d, t;\n @q add.rn.f64 %0, %0, d;\n}"
-        : "+d"(acc)
-        : "r"(u), "r"(h), "f"(vv), "f"(xv));
-}
-
 // acc += v * x: fused for f64; for f32 the product is rounded in f32 (as the
 // reference forms it) and accumulated in f64.  Empty slots add exact zeros.
 template <typename T>
@@ -269,13 +236,11 @@ __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h
     T vv[U][NS], xv[U][NS];
     uint32_t vtop[U];  // value of the block's highest remaining bit; slot u reads vtop - u
     int h0[U];
-    const T *xb[U];
 #pragma unroll
     for (int k = 0; k < U; ++k) {
         h0[k] = h[k];
         vtop[k] = vaddr[k] + (uint32_t)(h[k] - 1) * (uint32_t)sizeof(T);
-        h[k] = max(h[k] - NS, 0);  // >= 0 keeps empty slots' loads inside the slot
-        xb[k] = x + col[k];
+        h[k] = max(h[k] - NS, 0);
     }
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
@@ -283,16 +248,15 @@ __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h
         for (int k = 0; k < U; ++k) {
             const uint32_t pos = bfind(m[k]);
             m[k] &= ~(1u << pos);
-            xv[k][u] = ldg_pred(xb[k] + pos, u < h0[k]);
-            // an empty slot's value load stays inside the slot (the masks
-            // precede the values); its product is skipped
-            vv[k][u] = lds_val<T>(vtop[k] - (uint32_t)(u * sizeof(T)));
+            const bool ok = u < h0[k];
+            xv[k][u] = ldg_pred(x + (col[k] + pos), ok);
+            vv[k][u] = lds_pred<T>(vtop[k] - (uint32_t)(u * sizeof(T)), ok);
         }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
 #pragma unroll
-        for (int u = 0; u < NS; ++u) slot_mac<T>(acc, vv[k][u], xv[k][u], u, h0[k]);
+        for (int u = 0; u < NS; ++u) mac<T>(acc, vv[k][u], xv[k][u]);
     }
 }
 
