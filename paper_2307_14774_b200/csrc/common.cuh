@@ -43,9 +43,8 @@ struct Plan {
     int64_t num_granules = 0;
     uint32_t *pstart_bits = nullptr;  // [num_granules] bit i of word g: block 32g-off32+i starts a panel
     uint8_t *chunk_flags = nullptr;   // [num_chunks] bit0: starts inside a panel, bit1: has empty panels
-    // lane-per-panel chunks: record of panel p (chunk c) at p + c: first block
-    // (bits 0-15) and first value (bits 16-31) relative to the chunk start
-    uint32_t *lpr_rec = nullptr;      // [num_panels + num_chunks + 2]
+    uint8_t *blob = nullptr;          // per-chunk metadata blobs (plan.cu blob_fill_kernel)
+    uint4 *issue_rec = nullptr;       // [2*num_chunks] bulk-copy sources/sizes per chunk
 };
 
 struct Matrix {

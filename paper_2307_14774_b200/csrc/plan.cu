@@ -258,25 +258,70 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
     flags[c] = f;
 }
 
-// panel records of lane-per-panel chunks (warp per chunk): for q = 0..npc,
-// rec[p0 + q + c] = (rowptr[p0+q] - b0) | (values before panel p0+q in the chunk) << 16
-__global__ void lpr_rec_kernel(int64_t nc, int r, int vs, const int64_t *__restrict__ chunk_b,
-                               const int64_t *__restrict__ chunk_p,
-                               const uint8_t *__restrict__ flags, const int64_t *__restrict__ rowptr,
-                               const void *__restrict__ masks, uint32_t *rec) {
+// Per-chunk metadata blob (what K2 stages first into a ring slot):
+//   [0,64)  header: b0, b1, v0, p0, pe (int64), flags, rec offset (int32)
+//   [64,..) panel-start words of granules (b0+off32)>>5 .. (b1-1+off32)>>5
+//           (scan-mode chunks only)
+//   [rec,.) lane-per-panel chunks: for q = 0..npc the record
+//           (rowptr[p0+q] - b0) | (values before panel p0+q in the chunk) << 16
+__device__ __forceinline__ void blob_shape(int64_t b0, int64_t b1, int64_t npc, int flags,
+                                           int off32, int64_t *nwords, int64_t *nrec) {
+    const bool lpr = flags & 4;
+    *nwords = (!lpr && b1 > b0) ? ((b1 - 1 + off32) >> 5) - ((b0 + off32) >> 5) + 1 : 0;
+    *nrec = lpr ? npc + 1 : 0;
+}
+__device__ __forceinline__ int64_t a16_dev(int64_t v) { return (v + 15) / 16 * 16; }
+
+__global__ void blob_size_kernel(int64_t nc, const int64_t *__restrict__ chunk_b,
+                                 const int64_t *__restrict__ chunk_p,
+                                 const uint8_t *__restrict__ flags, int off32, int64_t *size16) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    int64_t nw, nr;
+    blob_shape(chunk_b[c], chunk_b[c + 1], chunk_p[c + 1] - chunk_p[c], flags[c], off32, &nw, &nr);
+    size16[c] = (64 + a16_dev(nw * 4) + a16_dev(nr * 4)) / 16;
+}
+
+// warp per chunk: header, panel-start words, panel records
+__global__ void blob_fill_kernel(int64_t nc, int r, int vs, int off32,
+                                 const int64_t *__restrict__ chunk_b,
+                                 const int64_t *__restrict__ chunk_v,
+                                 const int64_t *__restrict__ chunk_p,
+                                 const uint8_t *__restrict__ flags,
+                                 const int64_t *__restrict__ rowptr, const void *__restrict__ masks,
+                                 const uint32_t *__restrict__ pstart_bits,
+                                 const int64_t *__restrict__ off16_incl, uint8_t *blob) {
     const int lane = threadIdx.x & 31;
     const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
     const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
     for (int64_t c = warp; c < nc; c += nwarps) {
-        if (!(flags[c] & 4)) continue;
-        const int64_t b0 = chunk_b[c], p0 = chunk_p[c];
-        const int64_t npc = chunk_p[c + 1] - p0;
+        const int64_t b0 = chunk_b[c], b1 = chunk_b[c + 1], p0 = chunk_p[c], pe = chunk_p[c + 1];
+        const int f = flags[c];
+        int64_t nw, nr;
+        blob_shape(b0, b1, pe - p0, f, off32, &nw, &nr);
+        uint8_t *bl = blob + (c ? off16_incl[c - 1] : 0) * 16;
+        const int rec_off = (int)(64 + a16_dev(nw * 4));
+        if (lane == 0) {
+            int64_t *h = reinterpret_cast<int64_t *>(bl);
+            h[0] = b0;
+            h[1] = b1;
+            h[2] = chunk_v[c];
+            h[3] = p0;
+            h[4] = pe;
+            reinterpret_cast<int *>(bl)[10] = f;
+            reinterpret_cast<int *>(bl)[11] = rec_off;
+            h[6] = h[7] = 0;
+        }
+        uint32_t *words = reinterpret_cast<uint32_t *>(bl + 64);
+        const int64_t g0 = (b0 + off32) >> 5;
+        for (int64_t i = lane; i < nw; i += 32) words[i] = pstart_bits[g0 + i];
+        uint32_t *rec = reinterpret_cast<uint32_t *>(bl + rec_off);
         uint32_t running = 0;
-        for (int64_t q0 = 0; q0 <= npc; q0 += 32) {
+        for (int64_t q0 = 0; q0 < nr; q0 += 32) {
             const int64_t q = q0 + lane;
-            const int64_t s = q <= npc ? rowptr[p0 + q] - b0 : 0;
+            const int64_t s = q < nr ? rowptr[p0 + q] - b0 : 0;
             int cnt = 0;
-            if (q < npc)
+            if (q < nr - 1)
                 for (int64_t b = rowptr[p0 + q]; b < rowptr[p0 + q + 1]; ++b)
                     for (int rr = 0; rr < r; ++rr) cnt += __popc(load_mask(masks, b * r + rr, vs));
             int incl = cnt;
@@ -284,11 +329,35 @@ __global__ void lpr_rec_kernel(int64_t nc, int r, int vs, const int64_t *__restr
                 const int t = __shfl_up_sync(0xffffffffu, incl, d);
                 if (lane >= d) incl += t;
             }
-            if (q <= npc)
-                rec[p0 + q + c] = (uint32_t)s | ((running + (uint32_t)(incl - cnt)) << 16);
+            if (q < nr) rec[q] = (uint32_t)s | ((running + (uint32_t)(incl - cnt)) << 16);
             running += (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
         }
     }
+}
+
+// the producer's view of a chunk: source offsets and sizes of its bulk copies
+// in 16-byte units (blob, column starts, masks, values) and the byte total
+__global__ void issue_rec_kernel(int64_t nc, int lb, int vb, const int64_t *__restrict__ chunk_b,
+                                 const int64_t *__restrict__ chunk_v,
+                                 const int64_t *__restrict__ off16_incl, uint4 *ir) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const int64_t b0 = chunk_b[c], b1 = chunk_b[c + 1], v0 = chunk_v[c], v1 = chunk_v[c + 1];
+    const int64_t m0 = c ? off16_incl[c - 1] : 0, mb = off16_incl[c] - m0;
+    const int64_t c0 = (b0 * 4) >> 4, cb = ((b1 * 4 + 15) >> 4) - c0;
+    const int64_t k0 = (b0 * lb) >> 4, kb = ((b1 * lb + 15) >> 4) - k0;
+    const int64_t q0 = (v0 * vb) >> 4, qb = v1 > v0 ? ((v1 * vb + 15) >> 4) - q0 : 0;
+    uint4 A, B;
+    A.x = (uint32_t)m0;
+    A.y = (uint32_t)c0;
+    A.z = (uint32_t)k0;
+    A.w = (uint32_t)q0;
+    B.x = (uint32_t)mb | ((uint32_t)cb << 16);
+    B.y = (uint32_t)kb | ((uint32_t)qb << 16);
+    B.z = (uint32_t)((mb + cb + kb + qb) * 16);
+    B.w = 0;
+    ir[2 * c] = A;
+    ir[2 * c + 1] = B;
 }
 
 // largest panel count of a lane-per-panel chunk (sizes the staged records)
@@ -399,7 +468,8 @@ void free_plan(Plan &p) {
     dev_free(p.tile_prefix);
     dev_free(p.pstart_bits);
     dev_free(p.chunk_flags);
-    dev_free(p.lpr_rec);
+    dev_free(p.blob);
+    dev_free(p.issue_rec);
     delete[] p.h_chunk_b;
     p = Plan{};
 }
@@ -612,7 +682,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.chunk_target = cb;
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
         const int64_t mb = P.max_chunk_blocks;
-        P.lay_rp = 64 + a16((mb / 32 + 2) * 4 + 32);  // 64-byte chunk header, then bits
+        // slot: metadata blob (header, words, records), then the matrix arrays
+        P.lay_rp = 64 + a16((mb / 32 + 2) * 4 + 32);
         P.lay_col = P.lay_rp + (P.max_lpp_panels ? a16((P.max_lpp_panels + 1) * 4 + 32) : 0);
         P.lay_mask = P.lay_col + a16(mb * 4 + 32);
         P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);
@@ -626,14 +697,6 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     }
     if (P.slot_bytes > 14 * 1024)
         return fail(SPC5_EINVAL, "a chunk of this matrix does not fit the shared-memory ring");
-    // panel records of the lane-per-panel chunks
-    if (P.max_lpp_panels) {
-        SPC5_TRY(dev_alloc(&P.lpr_rec, (size_t)(np + P.num_chunks + 2)));
-        lpr_rec_kernel<<<(unsigned)std::min<int64_t>(cdiv(P.num_chunks, 8), 65535), 256, 0, st>>>(
-            P.num_chunks, m.r, m.vs, P.chunk_b, P.chunk_p, P.chunk_flags, m.rowptr, m.masks,
-            P.lpr_rec);
-        SPC5_CUDA(cudaGetLastError());
-    }
     // panel-start bitmap
     const int off32 = (int)(((m.block_base % 32) + 32) % 32);
     const int64_t ng = cdiv(nb + off32, 32);
@@ -643,7 +706,34 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     pstart_bits_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, off32,
                                                                  P.pstart_bits);
     SPC5_CUDA(cudaGetLastError());
-    SPC5_CUDA(cudaStreamSynchronize(st));
+    // per-chunk metadata blobs and issue records
+    const int64_t nc = P.num_chunks;
+    if (nc) {
+        int64_t *size16 = nullptr, *off16 = nullptr;
+        SPC5_TRY(dev_alloc(&size16, (size_t)nc));
+        SPC5_TRY(dev_alloc(&off16, (size_t)nc));
+        blob_size_kernel<<<(unsigned)cdiv(nc, 256), 256, 0, st>>>(nc, P.chunk_b, P.chunk_p,
+                                                                   P.chunk_flags, off32, size16);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_TRY(scan_inclusive_i64(size16, off16, nc, st));
+        int64_t total16 = 0;
+        SPC5_CUDA(cudaMemcpyAsync(&total16, off16 + nc - 1, sizeof(int64_t),
+                                  cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        if (total16 >= (int64_t(1) << 32)) return fail(SPC5_ENOMEM, "chunk metadata too large");
+        SPC5_TRY(dev_alloc(&P.blob, (size_t)total16 * 16));
+        blob_fill_kernel<<<(unsigned)std::min<int64_t>(cdiv(nc, 8), 65535), 256, 0, st>>>(
+            nc, m.r, m.vs, off32, P.chunk_b, P.chunk_v, P.chunk_p, P.chunk_flags, m.rowptr,
+            m.masks, P.pstart_bits, off16, P.blob);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_TRY(dev_alloc(&P.issue_rec, (size_t)nc * 2));
+        issue_rec_kernel<<<(unsigned)cdiv(nc, 256), 256, 0, st>>>(
+            nc, m.r * m.mask_bytes(), m.value_bytes(), P.chunk_b, P.chunk_v, off16, P.issue_rec);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(size16);
+        dev_free(off16);
+    }
     P.built = true;
     return SPC5_OK;
 }

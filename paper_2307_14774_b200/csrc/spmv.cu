@@ -54,9 +54,9 @@ struct SpmvArgs {
     int64_t num_empty;
     int off32;         // block_base mod 32 (window alignment)
     int accumulate;
-    uint32_t lay_rp, lay_col, lay_mask, lay_val, lay_bytes;  // slot layout (bytes)
-    int max_rp;        // panel ends staged for lane-per-panel chunks
-    const uint32_t *lpr_rec;  // lane-per-panel chunks: per panel (block, value) offsets
+    uint32_t lay_col, lay_mask, lay_val, lay_bytes;  // slot layout (bytes)
+    const uint8_t *blob;      // per-chunk metadata blobs (header, panel-start words, records)
+    const uint4 *issue_rec;   // per chunk: bulk-copy sources / sizes (plan.cu issue_rec_kernel)
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -286,70 +286,30 @@ __device__ __forceinline__ void row_dispatch(double &acc, uint32_t (&m)[U], int 
     }
 }
 
-__device__ __forceinline__ uint64_t align_dn16(uint64_t v) { return v & ~uint64_t(15); }
-__device__ __forceinline__ uint64_t align_up16(uint64_t v) { return (v + 15) & ~uint64_t(15); }
 
-// Chunk descriptor spread over lanes 0..6 (one int64 field per lane):
-// b0, b1 (blocks), v0, v1 (values), p0 (panel of b0), pe (panel of b1), flags.
-// Loaded two chunks ahead so its latency hides behind the current chunk.
-__device__ __forceinline__ int64_t desc_load(const SpmvArgs &a, int64_t c, bool valid, int lane) {
-    if (!valid || lane > 6) return 0;
-    if (lane == 6) return (int64_t)a.chunk_flags[c];
-    const int64_t *base = lane < 2 ? a.chunk_b : (lane < 4 ? a.chunk_v : a.chunk_p);
-    return __ldg(base + c + (lane & 1));
-}
-struct ChunkDesc {
-    int64_t b0, b1, v0, v1, p0, pe;
-    int flags;
-};
-__device__ __forceinline__ ChunkDesc desc_get(int64_t d) {
-    ChunkDesc r;
-    r.b0 = __shfl_sync(kFull, d, 0);
-    r.b1 = __shfl_sync(kFull, d, 1);
-    r.v0 = __shfl_sync(kFull, d, 2);
-    r.v1 = __shfl_sync(kFull, d, 3);
-    r.p0 = __shfl_sync(kFull, d, 4);
-    r.pe = __shfl_sync(kFull, d, 5);
-    r.flags = (int)__shfl_sync(kFull, d, 6);
-    return r;
-}
 
-// Lane 0 of the warp: copy one chunk (panel-start words, [panel records for
-// lane-per-panel chunks], column starts, masks, values) into the slot at
-// shared address `slot` with bulk copies that complete on one mbarrier.
+// Lane 0 of the warp: copy one chunk into the slot at shared address `slot`
+// with bulk copies completing on one mbarrier: its metadata blob (header,
+// panel-start words or panel records), column starts, masks and values.
+// The plan precomputed every source offset and size (16-byte units).
 template <typename T, int LB>
-__device__ __forceinline__ void issue_chunk(const SpmvArgs &a, const ChunkDesc &d, int64_t c,
-                                            uint32_t slot, uint64_t *bar, uint64_t pol) {
-    const uint64_t w0 = (uint64_t)(a.pstart_bits + ((d.b0 + a.off32) >> 5));
-    const uint64_t w1 = (uint64_t)(a.pstart_bits + ((d.b1 - 1 + a.off32) >> 5) + 1);
-    const uint64_t c0 = (uint64_t)(a.colidx + d.b0), c1 = (uint64_t)(a.colidx + d.b1);
-    const uint64_t m0 = (uint64_t)((const uint8_t *)a.masks + d.b0 * LB);
-    const uint64_t m1 = (uint64_t)((const uint8_t *)a.masks + d.b1 * LB);
-    const uint64_t q0 = (uint64_t)((const T *)a.values + d.v0);
-    const uint64_t q1 = (uint64_t)((const T *)a.values + d.v1);
-    const uint32_t bw = (uint32_t)(align_up16(w1) - align_dn16(w0));
-    const uint32_t bc = (uint32_t)(align_up16(c1) - align_dn16(c0));
-    const uint32_t bm = (uint32_t)(align_up16(m1) - align_dn16(m0));
-    const uint32_t bv = d.v1 > d.v0 ? (uint32_t)(align_up16(q1) - align_dn16(q0)) : 0u;
-    uint32_t br = 0;
-    uint64_t r0 = 0;
-    if (d.flags & 4) {  // panel records p0 .. pe (stored at p0 + c)
-        r0 = (uint64_t)(a.lpr_rec + d.p0 + c);
-        br = (uint32_t)(align_up16((uint64_t)(a.lpr_rec + d.pe + c + 1)) - align_dn16(r0));
+__device__ __forceinline__ void issue_chunk(const SpmvArgs &a, uint4 A, uint4 B, uint32_t slot,
+                                            uint64_t *bar, uint64_t pol) {
+    const uint8_t *colb = reinterpret_cast<const uint8_t *>(a.colidx);
+    const uint8_t *maskb = static_cast<const uint8_t *>(a.masks);
+    const uint8_t *valb = static_cast<const uint8_t *>(a.values);
+    mbar_expect_tx(bar, B.z);
+    bulk_g2s(slot, a.blob + (size_t)A.x * 16, (B.x & 0xffffu) * 16, bar, pol);
+    bulk_g2s(slot + a.lay_col, colb + (size_t)A.y * 16, (B.x >> 16) * 16, bar, pol);
+    bulk_g2s(slot + a.lay_mask, maskb + (size_t)A.z * 16, (B.y & 0xffffu) * 16, bar, pol);
+    if (B.y >> 16) bulk_g2s(slot + a.lay_val, valb + (size_t)A.w * 16, (B.y >> 16) * 16, bar, pol);
+}
+__device__ __forceinline__ void ir_load(const SpmvArgs &a, int64_t c, bool valid, uint4 &A,
+                                        uint4 &B) {
+    if (valid) {
+        A = __ldg(a.issue_rec + 2 * c);
+        B = __ldg(a.issue_rec + 2 * c + 1);
     }
-    // slot header for the consumer: b0, b1, v0, p0, pe, flags
-    asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(slot), "l"(d.b0), "l"(d.b1) : "memory");
-    asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(slot + 16), "l"(d.v0), "l"(d.p0)
-                 : "memory");
-    asm volatile("st.shared.v2.s64 [%0], {%1, %2};" ::"r"(slot + 32), "l"(d.pe),
-                 "l"((int64_t)d.flags)
-                 : "memory");
-    mbar_expect_tx(bar, bw + br + bc + bm + bv);
-    bulk_g2s(slot + kHdr, (const void *)align_dn16(w0), bw, bar, pol);
-    if (br) bulk_g2s(slot + a.lay_rp, (const void *)align_dn16(r0), br, bar, pol);
-    bulk_g2s(slot + a.lay_col, (const void *)align_dn16(c0), bc, bar, pol);
-    bulk_g2s(slot + a.lay_mask, (const void *)align_dn16(m0), bm, bar, pol);
-    if (bv) bulk_g2s(slot + a.lay_val, (const void *)align_dn16(q0), bv, bar, pol);
 }
 
 __device__ __forceinline__ int64_t lds_s64(uint32_t addr) {
@@ -516,17 +476,12 @@ __global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs 
     const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * wpc + warp;
     const int64_t c_end = a.c_hi;
     // prologue: fill the ring with the warp's first two chunks
-    {
-        const int64_t d0 = desc_load(a, cfirst, cfirst < c_end, lane);
-        const int64_t d1 = desc_load(a, cfirst + stride, cfirst + stride < c_end, lane);
-        if (cfirst < c_end) {
-            const ChunkDesc d = desc_get(d0);
-            if (lane == 0) issue_chunk<T, LB>(a, d, cfirst, ring, bars, pol);
-        }
-        if (cfirst + stride < c_end) {
-            const ChunkDesc d = desc_get(d1);
-            if (lane == 0) issue_chunk<T, LB>(a, d, cfirst + stride, ring + a.lay_bytes, bars + 1, pol);
-        }
+    if (lane == 0) {
+        uint4 A0, B0, A1, B1;
+        ir_load(a, cfirst, cfirst < c_end, A0, B0);
+        ir_load(a, cfirst + stride, cfirst + stride < c_end, A1, B1);
+        if (cfirst < c_end) issue_chunk<T, LB>(a, A0, B0, ring, bars, pol);
+        if (cfirst + stride < c_end) issue_chunk<T, LB>(a, A1, B1, ring + a.lay_bytes, bars + 1, pol);
     }
 
     uint32_t it = 0;
@@ -535,14 +490,16 @@ __global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs 
         const uint32_t parity = (it / kSlots) & 1u;
         // descriptor of the chunk this slot is refilled with at the end of the
         // iteration: loaded now, its latency hides behind this chunk's work
-        const int64_t dnext = desc_load(a, c + 2 * stride, c + 2 * stride < c_end, lane);
+        uint4 nA, nB;  // issue record of the chunk that refills this slot
+        ir_load(a, c + 2 * stride, lane == 0 && c + 2 * stride < c_end, nA, nB);
         const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
         mbar_wait(bars + slot_i, parity);
         // this chunk's descriptor, written into the slot header by the producer
         const int64_t b0 = lds_s64(sbase), b1 = lds_s64(sbase + 8);
         const int64_t v0 = lds_s64(sbase + 16), p0 = lds_s64(sbase + 24);
         const int64_t pe = lds_s64(sbase + 32);
-        const int flags = (int)lds_s64(sbase + 40);
+        const int flags = (int)lds_u32(sbase + 40);
+        const uint32_t rec_off = lds_u32(sbase + 44);
 #ifdef SPC5_K2_STREAM_ONLY  // experiment: stream the matrix, skip the products
         if (b1 >= b0) {
             if (b1 > b0 + 1000000) y[0] = (T)v0;
@@ -560,8 +517,8 @@ __global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs 
             a1 = (int)(min(b1, a.b_hi) - b0);
         }
         // arrays are 256-byte aligned: a region's offset in its slot is its start mod 16
-        const uint32_t a_bits = sbase + kHdr + (uint32_t)((((b0 + a.off32) >> 5) * 4) & 15);
-        const uint32_t a_rp = sbase + a.lay_rp + (uint32_t)(((p0 + c) * 4) & 15);
+        const uint32_t a_bits = sbase + kHdr;  // words from granule (b0 + off32) >> 5
+        const uint32_t a_rp = sbase + rec_off;
         const uint32_t a_col = sbase + a.lay_col + (uint32_t)((b0 * 4) & 15);
         const uint32_t a_mask = sbase + a.lay_mask + (uint32_t)((b0 * LB) & 15);
         const uint32_t a_val = sbase + a.lay_val + (uint32_t)((v0 * (int64_t)sizeof(T)) & 15);
@@ -683,13 +640,9 @@ __global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs 
         }
         // ---- release the slot and refill it with the chunk kSlots ahead
         __syncwarp();
-        const int64_t cn = c + 2 * stride;
-        if (cn < c_end) {
-            const ChunkDesc d2 = desc_get(dnext);
-            if (lane == 0) {
-                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-                issue_chunk<T, LB>(a, d2, cn, sbase, bars + slot_i, pol);
-            }
+        if (lane == 0 && c + 2 * stride < c_end) {
+            asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+            issue_chunk<T, LB>(a, nA, nB, sbase, bars + slot_i, pol);
         }
     }
 }
@@ -791,13 +744,13 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
     a.chunk_p = P.chunk_p;
     a.chunk_flags = P.chunk_flags;
     a.pstart_bits = P.pstart_bits;
-    a.lpr_rec = P.lpr_rec;
+    a.blob = P.blob;
+    a.issue_rec = P.issue_rec;
     a.carry = P.carry;
     a.empty_panels = P.empty_panels;
     a.num_empty = P.num_empty;
     a.off32 = (int)(((m.block_base % 32) + 32) % 32);
     a.accumulate = accumulate;
-    a.lay_rp = (uint32_t)P.lay_rp;
     a.lay_col = (uint32_t)P.lay_col;
     a.lay_mask = (uint32_t)P.lay_mask;
     a.lay_val = (uint32_t)P.lay_val;
