@@ -57,12 +57,13 @@ struct SpmvArgs {
     uint32_t lay_col, lay_mask, lay_val, lay_bytes;  // slot layout (bytes)
     const uint8_t *blob;      // per-chunk metadata blobs (header, panel-start words, records)
     const uint4 *issue_rec;   // per chunk: bulk-copy sources / sizes (plan.cu issue_rec_kernel)
+    int nslot;                // ring slots per warp (2..kMaxSlots)
 };
 
 constexpr unsigned kFull = 0xffffffffu;
-constexpr int kSlots = 2;    // chunks in flight per warp
+constexpr int kMaxSlots = 4;  // ring slots per warp (SpmvArgs::nslot)
 constexpr uint32_t kHdr = 64;  // slot header bytes (chunk descriptor)
-constexpr uint32_t kRingOff = 128;  // barriers before the ring
+constexpr uint32_t kRingOff = 256;  // barriers (8 warps x kMaxSlots) before the ring
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -233,7 +234,7 @@ template <typename T, int U, int NS>
 __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h)[U],
                                           const T *__restrict__ x, const uint32_t (&col)[U],
                                           const uint32_t (&vaddr)[U]) {
-    T vv[U][NS], xv[U][NS];
+    T xv[U][NS];
     uint32_t vtop[U];  // value of the block's highest remaining bit; slot u reads vtop - u
     int h0[U];
 #pragma unroll
@@ -242,21 +243,23 @@ __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h
         vtop[k] = vaddr[k] + (uint32_t)(h[k] - 1) * (uint32_t)sizeof(T);
         h[k] = max(h[k] - NS, 0);
     }
+    // all x gathers first (the long-latency loads), then values and products
 #pragma unroll
     for (int u = 0; u < NS; ++u) {
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             const uint32_t pos = bfind(m[k]);
             m[k] &= ~(1u << pos);
-            const bool ok = u < h0[k];
-            xv[k][u] = ldg_pred(x + (col[k] + pos), ok);
-            vv[k][u] = lds_pred<T>(vtop[k] - (uint32_t)(u * sizeof(T)), ok);
+            xv[k][u] = ldg_pred(x + (col[k] + pos), u < h0[k]);
         }
     }
 #pragma unroll
     for (int k = 0; k < U; ++k) {
 #pragma unroll
-        for (int u = 0; u < NS; ++u) mac<T>(acc, vv[k][u], xv[k][u]);
+        for (int u = 0; u < NS; ++u) {
+            const T vv = lds_pred<T>(vtop[k] - (uint32_t)(u * sizeof(T)), u < h0[k]);
+            mac<T>(acc, vv, xv[k][u]);
+        }
     }
 }
 
@@ -350,9 +353,38 @@ __device__ __forceinline__ uint32_t row_rt(const LaneMasks<LB> &mk, int rr) {
 // matrices).  The plan's panel records give each panel's first block and
 // first value inside the chunk (16 bits each), so a lane starts at once;
 // with G > 1 the lanes of a row also count their sub-ranges' values.
-#ifndef SPC5_LPP_U
-#define SPC5_LPP_U 3
-#endif
+// Lane's row over blocks s .. s+my-1 of its panel range, U blocks per step.
+template <typename T, typename MT, int R, int U>
+__device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s, int rr,
+                                          uint32_t vaddr, uint32_t a_col, uint32_t a_mask,
+                                          const T *__restrict__ x) {
+    constexpr int MB = (int)sizeof(MT);
+    constexpr int LB = R * MB;
+    for (int j = 0; j < maxlen; j += U) {
+        uint32_t col[U], vr[U], m[U];
+        int h[U], cm = 0;
+        uint32_t vnext = vaddr;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const bool ok = j + k < my;
+            const uint32_t bk = (uint32_t)(ok ? s + j + k : 0);
+            col[k] = lds_u32(a_col + bk * 4u);
+            LaneMasks<LB> mk;
+            mk.load(a_mask + bk * LB);
+            mk.clear_if(ok);
+            // block k's values: rows 0..R-1 in order; this lane's row starts
+            // after the rows below it
+            vr[k] = vnext + (uint32_t)popc_below<LB, MB>(mk, rr) * (uint32_t)sizeof(T);
+            vnext += (uint32_t)mk.popc() * (uint32_t)sizeof(T);
+            m[k] = R == 1 ? mk.w[0] : row_rt<LB, MB>(mk, rr);
+            h[k] = __popc(m[k]);
+            cm = max(cm, h[k]);
+        }
+        vaddr = vnext;
+        row_dispatch<T, U>(acc, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
+    }
+}
+
 template <typename T, typename MT, int R, bool GENERIC>
 __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t p0, int npc, int lg,
                                           uint32_t a_rec, uint32_t a_col, uint32_t a_mask,
@@ -396,31 +428,15 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t p0, int npc
         const int maxlen = __reduce_max_sync(kFull, my);
         uint32_t vaddr = a_val + vofs * (uint32_t)sizeof(T);
         double acc = 0.0;
-        // U blocks per step: all their x gathers are in flight before the
-        // first FMA (values still accumulate in storage order)
-        constexpr int U = SPC5_LPP_U;
-        for (int j = 0; j < maxlen; j += U) {
-            uint32_t col[U], vr[U], m[U];
-            int h[U], cm = 0;
-            uint32_t vnext = vaddr;
-#pragma unroll
-            for (int k = 0; k < U; ++k) {
-                const bool ok = j + k < my;
-                const uint32_t bk = (uint32_t)(ok ? s + j + k : 0);
-                col[k] = lds_u32(a_col + bk * 4u);
-                LaneMasks<LB> mk;
-                mk.load(a_mask + bk * LB);
-                mk.clear_if(ok);
-                // block k's values: rows 0..R-1 in order; this lane's row starts
-                // after the rows below it
-                vr[k] = vnext + (uint32_t)popc_below<LB, MB>(mk, rr) * (uint32_t)sizeof(T);
-                vnext += (uint32_t)mk.popc() * (uint32_t)sizeof(T);
-                m[k] = R == 1 ? mk.w[0] : row_rt<LB, MB>(mk, rr);
-                h[k] = __popc(m[k]);
-                cm = max(cm, h[k]);
-            }
-            vaddr = vnext;
-            row_dispatch<T, U>(acc, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
+        // U blocks per step (U from the longest lane range): all their x
+        // gathers are in flight before the first FMA; values still accumulate
+        // in storage order
+        if (maxlen <= 3) {
+            lpp_steps<T, MT, R, 3>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, x);
+        } else if (maxlen <= 6) {
+            lpp_steps<T, MT, R, 6>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, x);
+        } else {
+            lpp_steps<T, MT, R, 9>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, x);
         }
         for (int o = 1; o < G; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
         const int64_t p = p0 + q;
@@ -437,10 +453,12 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t p0, int npc
 // GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
 // spmv_parallel); the arithmetic per panel is identical.
 template <typename T, typename MT, int R, bool GENERIC>
-#ifndef SPC5_K2_MINB
-#define SPC5_K2_MINB 2
+// 168 registers: 12 warps per SM (3 CTAs x 4 warps) fit the register file;
+// the shared-memory ring allows no more
+#ifndef SPC5_K2_MAXREG
+#define SPC5_K2_MAXREG 168
 #endif
-__global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs a) {
+__global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;  // mask bytes per lane (<= 16)
     extern __shared__ __align__(128) uint8_t smem[];
@@ -450,11 +468,12 @@ __global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs 
     const T *__restrict__ x = static_cast<const T *>(a.x);
     T *__restrict__ y = static_cast<T *>(a.y);
 
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * kSlots;
-    const uint32_t ring = smem_addr(smem) + kRingOff + (uint32_t)(warp * kSlots) * a.lay_bytes;
+    const int S = a.nslot;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * kMaxSlots;
+    const uint32_t ring = smem_addr(smem) + kRingOff + (uint32_t)(warp * S) * a.lay_bytes;
     if (lane == 0) {
 #pragma unroll
-        for (int i = 0; i < kSlots; ++i) mbar_init(bars + i, 1);
+        for (int i = 0; i < S; ++i) mbar_init(bars + i, 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     }
     __syncwarp();
@@ -475,23 +494,24 @@ __global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs 
     const int64_t stride = (int64_t)gridDim.x * wpc;
     const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * wpc + warp;
     const int64_t c_end = a.c_hi;
-    // prologue: fill the ring with the warp's first two chunks
+    // prologue: fill the ring with the warp's first S chunks
     if (lane == 0) {
-        uint4 A0, B0, A1, B1;
-        ir_load(a, cfirst, cfirst < c_end, A0, B0);
-        ir_load(a, cfirst + stride, cfirst + stride < c_end, A1, B1);
-        if (cfirst < c_end) issue_chunk<T, LB>(a, A0, B0, ring, bars, pol);
-        if (cfirst + stride < c_end) issue_chunk<T, LB>(a, A1, B1, ring + a.lay_bytes, bars + 1, pol);
+        for (int i = 0; i < S; ++i) {
+            const int64_t ci = cfirst + i * stride;
+            if (ci >= c_end) break;
+            uint4 A, B;
+            ir_load(a, ci, true, A, B);
+            issue_chunk<T, LB>(a, A, B, ring + (uint32_t)i * a.lay_bytes, bars + i, pol);
+        }
     }
 
-    uint32_t it = 0;
-    for (int64_t c = cfirst; c < c_end; c += stride, ++it) {
-        const int slot_i = it % kSlots;
-        const uint32_t parity = (it / kSlots) & 1u;
-        // descriptor of the chunk this slot is refilled with at the end of the
-        // iteration: loaded now, its latency hides behind this chunk's work
-        uint4 nA, nB;  // issue record of the chunk that refills this slot
-        ir_load(a, c + 2 * stride, lane == 0 && c + 2 * stride < c_end, nA, nB);
+    int slot_i = 0;
+    uint32_t parity = 0;
+    for (int64_t c = cfirst; c < c_end; c += stride) {
+        const int64_t cn = c + S * stride;  // the chunk that refills this slot
+        // its issue record: loaded now, the latency hides behind this chunk's work
+        uint4 nA, nB;
+        ir_load(a, cn, lane == 0 && cn < c_end, nA, nB);
         const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
         mbar_wait(bars + slot_i, parity);
         // this chunk's descriptor, written into the slot header by the producer
@@ -638,11 +658,15 @@ __global__ void __launch_bounds__(256, SPC5_K2_MINB) spmv_kernel(const SpmvArgs 
         }
 
         }
-        // ---- release the slot and refill it with the chunk kSlots ahead
+        // ---- release the slot and refill it with the chunk S ahead
         __syncwarp();
-        if (lane == 0 && c + 2 * stride < c_end) {
+        if (lane == 0 && cn < c_end) {
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue_chunk<T, LB>(a, nA, nB, sbase, bars + slot_i, pol);
+        }
+        if (++slot_i == S) {
+            slot_i = 0;
+            parity ^= 1u;
         }
     }
 }
@@ -676,12 +700,15 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
 }
 
 template <typename K>
-int launch_ring_kernel(K kernel, const Matrix &m, const SpmvArgs &a, int64_t nslots,
+int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
                        cudaStream_t st) {
     // 8 warps per CTA for small slots; 4 for large ones so several CTAs share an SM
     int wpc = a.lay_bytes <= 6 * 1024 ? 8 : 4;
     if (const char *e = getenv("SPC5_WPC")) wpc = std::min(8, std::max(1, atoi(e)));  // tuning knob
-    const size_t smem = kRingOff + (size_t)wpc * kSlots * a.lay_bytes;  // barriers + ring
+    int S = 2;
+    if (const char *e = getenv("SPC5_NSLOT")) S = std::min(kMaxSlots, std::max(2, atoi(e)));
+    a.nslot = S;
+    const size_t smem = kRingOff + (size_t)wpc * S * a.lay_bytes;  // barriers + ring
     SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
     int per_sm = 0;
