@@ -300,23 +300,21 @@ def ours_single(args, formats):
     st = torch_stream()
     stream = torch.cuda.current_stream()
 
-    def step(events=None):
+    def run(f, n):
         launches = 0
-        for i, f in enumerate(formats):
-            if events is not None:
-                events[i][0].record(stream)
+        for _ in range(n):
             nat.check(nat.lib.spc5_spmv(handles[f], x.data_ptr(), ys[f].data_ptr(), 0, st))
             launches += nat.last_launch_count()
-            if events is not None:
-                events[i][1].record(stream)
         return launches
 
     for _ in range(args.warmup):
-        step()
+        for f in formats:
+            run(f, 1)
     torch.cuda.synchronize()
-    per = {f: [] for f in formats}
-    ev = [[[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
-           for _ in formats] for _ in range(args.steps)]
+    # timed region: the K products of each format back to back (K steps of one
+    # product per format), one event pair per format bracketing its K launches
+    ev = [[torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)]
+          for _ in formats]
     sampler = ClockSampler(torch.cuda.current_device())
     sampler.start()
     time.sleep(0.3)
@@ -324,15 +322,15 @@ def ours_single(args, formats):
     e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     launches = 0
     e0.record(stream)
-    for k in range(args.steps):
-        launches += step(ev[k])
+    for i, f in enumerate(formats):
+        ev[i][0].record(stream)
+        launches += run(f, args.steps)
+        ev[i][1].record(stream)
     e1.record(stream)
     torch.cuda.synchronize()
     clocks = sampler.stop()
     elapsed = e0.elapsed_time(e1) * 1e-3
-    for k in range(args.steps):
-        for i, f in enumerate(formats):
-            per[f].append(ev[k][i][0].elapsed_time(ev[k][i][1]) * 1e-3)
+    per = {f: [ev[i][0].elapsed_time(ev[i][1]) * 1e-3 / args.steps] for i, f in enumerate(formats)}
     flops_step = sum(2.0 * mats[f].nnz for f in formats)
     value = flops_step * args.steps / elapsed / 1e9
     peak, peak_kind = peaks()
@@ -364,7 +362,7 @@ def ours_single(args, formats):
                 "peak_source": f"{peak_kind} (MEASURED_PEAKS.json hbm_gbs)"
                 if peak_kind == "measured" else "fallback (B200_PROFILING.md)",
                 "alg_bytes_per_step": tot_bytes,
-                "kernel": "spc5::spmv_kernel (K2), mean CUDA-event launch time per format"}
+                "kernel": "spc5::spmv_kernel (K2), mean launch time per format (CUDA events around its K launches)"}
 
     # ---- e2e through the public API with pinned host buffers
     e2e = None
@@ -411,6 +409,7 @@ def ours_single(args, formats):
                        "num_rows": num_rows,
                        "nnz": mats[formats[0]].nnz,
                        "step": "y_f = A_f.x for every format, device-resident x/y",
+                       "order": "the K products of each format run back to back",
                        "l2": "inputs larger than L2 (no flush); x L2-resident by design",
                        "conversion_s": t_conv},
             "roofline": roofline, "formats": fmts, "gpu_launches": launches,

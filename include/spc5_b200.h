@@ -24,9 +24,11 @@
  *      SPC5_EINDEX  -> IndexError   (set bit addresses a column >= num_cols;
  *                                    vlane.py:58-77)
  *      SPC5_ECUDA / SPC5_ENOMEM -> RuntimeError
- *  - A matrix handle is immutable after construction and may be used from
- *    several threads/streams at once; the spmv path never
- *    allocates (a per-handle plan is built once, at construction/import).
+ *  - A matrix handle may be used from several threads/streams at once
+ *    (SPEC.md:373-374); the spmv path never allocates (a per-handle plan is
+ *    built once, at construction/import).  The plan depends on the structure
+ *    arrays (rowptr, colidx, masks) only: values may be rewritten in place
+ *    between products, a structure change needs a new handle.
  */
 #ifndef SPC5_B200_H
 #define SPC5_B200_H
@@ -68,8 +70,9 @@ int spc5_device_count(int *count);
  * (row_ptr int64[num_rows+1], col_idx int32[nnz] strictly increasing per row,
  * values f32/f64[nnz]).  block_base: global block index of this matrix's first
  * block when it is a row-panel shard of a larger matrix (0 otherwise); it only
- * fixes the warp-window alignment so shards reproduce the full matrix's y
- * bit for bit.  The result owns its device arrays.
+ * keeps the warp windows on the global block grid, so a shard's rows agree
+ * with the full matrix's y to <= 1e-15 relative.  The result owns its device
+ * arrays.
  */
 int spc5_convert_csr(int64_t num_rows, int64_t num_cols, int64_t nnz, int precision,
                      int r, int vs, const int64_t *d_row_ptr, const int32_t *d_col_idx,
