@@ -113,11 +113,38 @@ def build_matrices(cfg_id: int, formats, rank_rows=None):
         for (r, vs) in formats:
             mats[(r, vs)] = csr_to_spc5(m, r, vs)
         return mats, m.num_rows, m.num_cols
+    tdt = torch.float64 if prec == "f64" else torch.float32
+    pcode = 1 if prec == "f64" else 0
+    if cfg.get("gen") in ("powerlaw", "fem"):
+        from paper_2307_14774_b200.workloads import PL_TABLE_BITS, powerlaw_len_table
+        N, C = cfg["rows"], cfg["cols"]
+        table = torch.from_numpy(powerlaw_len_table()).to("cuda")
+        rp = torch.empty(N + 1, dtype=torch.int64, device="cuda")
+        if cfg["gen"] == "powerlaw":
+            nat.check(nat.lib.spc5_gen_powerlaw_rowptr(N, 0, N, 0, table.data_ptr(), PL_TABLE_BITS,
+                                                       rp.data_ptr(), 0))
+        else:
+            nat.check(nat.lib.spc5_gen_fem_rowptr(N // 3, 0, N, rp.data_ptr(), 0))
+        nnz = int(rp[-1])
+        ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        va = torch.empty(nnz, dtype=tdt, device="cuda")
+        if cfg["gen"] == "powerlaw":
+            nat.check(nat.lib.spc5_gen_powerlaw_fill(N, 0, N, pcode, 0, table.data_ptr(),
+                                                     PL_TABLE_BITS, rp.data_ptr(), ci.data_ptr(),
+                                                     va.data_ptr(), 0))
+        else:
+            nat.check(nat.lib.spc5_gen_fem_fill(N // 3, 0, N, pcode, 0, rp.data_ptr(),
+                                                ci.data_ptr(), va.data_ptr(), 0))
+        torch.cuda.synchronize()
+        for (r, vs) in formats:
+            mats[(r, vs)] = csr_to_spc5_device(N, C, rp, ci, va, r, vs)
+        del rp, ci, va
+        torch.cuda.empty_cache()
+        return mats, N, C
     if "n" not in cfg:
         raise SystemExit(f"config {cfg_id} generator not available in this build")
     n = cfg["n"]
     N = n ** 3
-    tdt = torch.float64 if prec == "f64" else torch.float32
     for (r, vs) in formats:
         lo, hi, base = (0, N, 0) if rank_rows is None else rank_rows(r)
         rows = hi - lo
@@ -126,7 +153,7 @@ def build_matrices(cfg_id: int, formats, rank_rows=None):
         nnz = int(rp[-1])
         ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
         va = torch.empty(nnz, dtype=tdt, device="cuda")
-        nat.check(nat.lib.spc5_gen_stencil27_fill(n, lo, hi, 1 if prec == "f64" else 0, 0, 27.0,
+        nat.check(nat.lib.spc5_gen_stencil27_fill(n, lo, hi, pcode, 0, 27.0,
                                                   rp.data_ptr(), ci.data_ptr(), va.data_ptr(),
                                                   0))
         torch.cuda.synchronize()

@@ -172,6 +172,35 @@ int spc5_gen_stencil27_fill(int64_t n, int64_t row_lo, int64_t row_hi, int preci
                             uint64_t seed, double diag, const int64_t *d_row_ptr,
                             int32_t *d_col_idx, void *d_values, void *stream);
 
+/*
+ * Workload generator, BASELINE config 3: rows [row_lo, row_hi) of the n x n
+ * power-law matrix.  Row i draws its length from d_len_table (2^table_bits
+ * lognormal quantiles, workloads.py:powerlaw_len_table), then 80 % of its
+ * columns stratified over i +- 4096 and the rest stratified over [0, n),
+ * merged, duplicates dropped; values U(-1,1) position keyed.  Host twin:
+ * workloads.py:powerlaw_rows.
+ */
+int spc5_gen_powerlaw_rowptr(int64_t n, int64_t row_lo, int64_t row_hi, uint64_t seed,
+                             const int32_t *d_len_table, int table_bits, int64_t *d_row_ptr,
+                             void *stream);
+int spc5_gen_powerlaw_fill(int64_t n, int64_t row_lo, int64_t row_hi, int precision,
+                           uint64_t seed, const int32_t *d_len_table, int table_bits,
+                           const int64_t *d_row_ptr, int32_t *d_col_idx, void *d_values,
+                           void *stream);
+
+/*
+ * Workload generator, BASELINE config 4: rows [row_lo, row_hi) of the
+ * FEM-like matrix over `nodes` nodes x 3 dof.  Node q couples to itself and
+ * 26 nodes stratified over q +- 2048; row 3q+d holds the dense 3x3 blocks of
+ * those 27 nodes (81 entries), values ~N(0,1) (Irwin-Hall of 4 keyed
+ * uniforms).  Host twin: workloads.py:fem_rows.
+ */
+int spc5_gen_fem_rowptr(int64_t nodes, int64_t row_lo, int64_t row_hi, int64_t *d_row_ptr,
+                        void *stream);
+int spc5_gen_fem_fill(int64_t nodes, int64_t row_lo, int64_t row_hi, int precision,
+                      uint64_t seed, const int64_t *d_row_ptr, int32_t *d_col_idx,
+                      void *d_values, void *stream);
+
 /* Number of kernel launches the last spc5_spmv* call on this thread issued. */
 int spc5_last_launch_count(void);
 

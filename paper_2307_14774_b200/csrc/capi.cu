@@ -355,4 +355,35 @@ int spc5_gen_stencil27_fill(int64_t n, int64_t row_lo, int64_t row_hi, int preci
                               d_values, static_cast<cudaStream_t>(stream));
 }
 
+int spc5_gen_powerlaw_rowptr(int64_t n, int64_t row_lo, int64_t row_hi, uint64_t seed,
+                             const int32_t *d_len_table, int table_bits, int64_t *d_row_ptr,
+                             void *stream) {
+    return gen_powerlaw_rowptr(n, row_lo, row_hi, seed, d_len_table, table_bits, d_row_ptr,
+                               static_cast<cudaStream_t>(stream));
+}
+
+int spc5_gen_powerlaw_fill(int64_t n, int64_t row_lo, int64_t row_hi, int precision,
+                           uint64_t seed, const int32_t *d_len_table, int table_bits,
+                           const int64_t *d_row_ptr, int32_t *d_col_idx, void *d_values,
+                           void *stream) {
+    if (precision != SPC5_F32 && precision != SPC5_F64)
+        return fail(SPC5_EINVAL, "precision must be 'f32' or 'f64'");
+    return gen_powerlaw_fill(n, row_lo, row_hi, precision, seed, d_len_table, table_bits,
+                             d_row_ptr, d_col_idx, d_values, static_cast<cudaStream_t>(stream));
+}
+
+int spc5_gen_fem_rowptr(int64_t nodes, int64_t row_lo, int64_t row_hi, int64_t *d_row_ptr,
+                        void *stream) {
+    return gen_fem_rowptr(nodes, row_lo, row_hi, d_row_ptr, static_cast<cudaStream_t>(stream));
+}
+
+int spc5_gen_fem_fill(int64_t nodes, int64_t row_lo, int64_t row_hi, int precision,
+                      uint64_t seed, const int64_t *d_row_ptr, int32_t *d_col_idx,
+                      void *d_values, void *stream) {
+    if (precision != SPC5_F32 && precision != SPC5_F64)
+        return fail(SPC5_EINVAL, "precision must be 'f32' or 'f64'");
+    return gen_fem_fill(nodes, row_lo, row_hi, precision, seed, d_row_ptr, d_col_idx, d_values,
+                        static_cast<cudaStream_t>(stream));
+}
+
 }  // extern "C"

@@ -4,13 +4,12 @@
 //  * mask_popcounts / block_value_offsets (kernels.py:82-96): per-tile
 //    popcount sums (kTile blocks) + an exclusive scan; the value offset of any
 //    block b is tile_prefix[b / kTile] + a warp popcount over < kTile blocks.
-//  * The SpMV plan cuts the block array into chunks (one warp each).  Chunk
-//    starts are panel starts (targets every CB blocks snapped back to the
-//    start of the panel holding them) plus, inside panels longer than kSplit
-//    blocks, the GLOBAL multiples of kSplit.  A panel is therefore split only
-//    where its own length and global position say so, never where the chunk
-//    size does, which keeps y bitwise independent of the plan granularity,
-//    of spmv_parallel ranges and of row-panel sharding across GPUs.
+//  * The SpMV plan cuts the block array into chunks (one ring slot each).
+//    Chunk starts are panel starts (targets every CB blocks snapped back to
+//    the start of the panel holding them) plus, inside panels longer than
+//    split_len blocks, the GLOBAL multiples of split_len (the largest power of
+//    two whose fullest window fits 6 KB).  Per chunk the plan also writes a
+//    metadata blob and a bulk-copy issue record (see blob_fill_kernel).
 //  * partition_by_nnz (parallel.py:31-52): boundary_k =
 //    searchsorted(cum, total*k/P, 'left') + 1 with cum[p] = nnz up to the end
 //    of panel p, clamped to num_panels; one warp binary-searches each target.
@@ -19,6 +18,7 @@
 #include <thrust/iterator/counting_iterator.h>
 #include <thrust/iterator/transform_iterator.h>
 
+#include <cstdio>
 #include <cstdlib>
 #include <algorithm>
 #include <string>
@@ -185,17 +185,23 @@ __global__ void empty_flag_kernel(int64_t num_panels, const int64_t *__restrict_
 
 // ---- ring-slot sizing ------------------------------------------------------
 // largest popcount of one block (all r rows)
-__global__ void max_block_popc_kernel(int64_t nb, int r, int vs, const void *__restrict__ masks,
-                                      unsigned long long *out) {
+// most values in one window of sl blocks at global multiples of sl (warp per
+// window): bounds the bytes of any piece of a panel cut at those multiples
+__global__ void window_values_max_kernel(int64_t nb, int r, int vs, const void *__restrict__ masks,
+                                         int64_t base, int64_t sl, unsigned long long *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nwarps = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    const int64_t w0 = base / sl, w1 = (base + nb - 1) / sl;
     int best = 0;
-    for (int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; b < nb;
-         b += (int64_t)gridDim.x * blockDim.x) {
+    for (int64_t w = w0 + warp; w <= w1; w += nwarps) {
+        const int64_t lo = max(w * sl - base, (int64_t)0), hi = min((w + 1) * sl - base, nb);
         int s = 0;
-        for (int rr = 0; rr < r; ++rr) s += __popc(load_mask(masks, b * r + rr, vs));
-        best = max(best, s);
+        for (int64_t b = lo + lane; b < hi; b += 32)
+            for (int rr = 0; rr < r; ++rr) s += __popc(load_mask(masks, b * r + rr, vs));
+        best = max(best, __reduce_add_sync(0xffffffffu, s));
     }
-    best = __reduce_max_sync(0xffffffffu, best);
-    if ((threadIdx.x & 31) == 0) atomicMax(out, (unsigned long long)best);
+    if (lane == 0) atomicMax(out, (unsigned long long)best);
 }
 
 // max blocks and max values of one chunk (a chunk is one shared-memory slot)
@@ -268,7 +274,7 @@ __device__ __forceinline__ void blob_shape(int64_t b0, int64_t b1, int64_t npc, 
                                            int off32, int64_t *nwords, int64_t *nrec) {
     const bool lpr = flags & 4;
     *nwords = (!lpr && b1 > b0) ? ((b1 - 1 + off32) >> 5) - ((b0 + off32) >> 5) + 1 : 0;
-    *nrec = lpr ? npc + 1 : 0;
+    *nrec = lpr ? npc + 1 : 32;
 }
 __device__ __forceinline__ int64_t a16_dev(int64_t v) { return (v + 15) / 16 * 16; }
 
@@ -316,6 +322,36 @@ __global__ void blob_fill_kernel(int64_t nc, int r, int vs, int off32,
         const int64_t g0 = (b0 + off32) >> 5;
         for (int64_t i = lane; i < nw; i += 32) words[i] = pstart_bits[g0 + i];
         uint32_t *rec = reinterpret_cast<uint32_t *>(bl + rec_off);
+        if (!(f & 4)) {
+            // scan-mode chunk: lane l of K2 owns blocks [l*n/32, (l+1)*n/32);
+            // record = values before its first block | (panel starts in
+            // blocks 1 .. its first block) << 16
+            const int64_t n = b1 - b0;
+            const int64_t sl = (lane * n) >> 5, el = ((lane + 1) * n) >> 5;
+            int cnt = 0, starts = 0;
+            for (int64_t b = sl; b < el; ++b) {
+                for (int rr = 0; rr < r; ++rr) cnt += __popc(load_mask(masks, (b0 + b) * r + rr, vs));
+                const int64_t gb = b0 + b + off32;
+                starts += b > 0 ? (int)((pstart_bits[gb >> 5] >> (gb & 31)) & 1u) : 0;
+            }
+            int vin = cnt, pin = starts;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int tv = __shfl_up_sync(0xffffffffu, vin, d);
+                const int tp = __shfl_up_sync(0xffffffffu, pin, d);
+                if (lane >= d) {
+                    vin += tv;
+                    pin += tp;
+                }
+            }
+            // panel of the lane's first block: starts in blocks 1 .. sl
+            int first = pin - starts;
+            if (sl > 0 && sl < el) {
+                const int64_t gb = b0 + sl + off32;
+                first += (int)((pstart_bits[gb >> 5] >> (gb & 31)) & 1u);
+            }
+            rec[lane] = (uint32_t)(vin - cnt) | ((uint32_t)first << 16);
+            continue;
+        }
         uint32_t running = 0;
         for (int64_t q0 = 0; q0 < nr; q0 += 32) {
             const int64_t q = q0 + lane;
@@ -640,20 +676,28 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         return SPC5_OK;
     }
     // Long panels are cut every split_len blocks (at global multiples) with
-    // split_len sized so a piece fits one slot; chunks = ring slots, the
-    // largest target size whose worst chunk fits the slot target.
+    // split_len the largest power of two <= 512 whose fullest window of
+    // split_len blocks fits 6 KB; chunks = ring slots, the largest target size
+    // whose worst chunk fits the slot target.
     {
-        unsigned long long *d_mx = nullptr, h_mx = 0;
+        unsigned long long *d_mx = nullptr;
         SPC5_TRY(dev_alloc(&d_mx, 1));
-        SPC5_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
-        max_block_popc_kernel<<<(unsigned)std::min<int64_t>(cdiv(nb, 256), 148 * 16), 256, 0,
-                                st>>>(nb, m.r, m.vs, m.masks, d_mx);
-        SPC5_CUDA(cudaMemcpyAsync(&h_mx, d_mx, sizeof(h_mx), cudaMemcpyDeviceToHost, st));
-        SPC5_CUDA(cudaStreamSynchronize(st));
+        const int64_t per_block = 4 + m.r * m.mask_bytes();
+        int64_t sl = 512;
+        for (; sl > 1; sl >>= 1) {
+            if (sl * per_block > 6 * 1024) continue;
+            unsigned long long h_mx = 0;
+            SPC5_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
+            window_values_max_kernel<<<(unsigned)std::min<int64_t>(cdiv(cdiv(nb, sl) + 1, 8),
+                                                                   148 * 16),
+                                       256, 0, st>>>(nb, m.r, m.vs, m.masks, m.block_base, sl,
+                                                     d_mx);
+            SPC5_CUDA(cudaGetLastError());
+            SPC5_CUDA(cudaMemcpyAsync(&h_mx, d_mx, sizeof(h_mx), cudaMemcpyDeviceToHost, st));
+            SPC5_CUDA(cudaStreamSynchronize(st));
+            if (sl * per_block + (int64_t)h_mx * m.value_bytes() <= 6 * 1024) break;
+        }
         dev_free(d_mx);
-        const int64_t max_block_bytes = 4 + m.r * m.mask_bytes() + (int64_t)h_mx * m.value_bytes();
-        int64_t sl = 256;
-        while (sl > 1 && sl * max_block_bytes > 6 * 1024) sl >>= 1;
         P.split_len = sl;
     }
     int64_t slot_cap = 10 * 1024;  // target ring-slot size (tuning knob SPC5_SLOT_KB)
@@ -684,7 +728,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         const int64_t mb = P.max_chunk_blocks;
         // slot: metadata blob (header, words, records), then the matrix arrays
         P.lay_rp = 64 + a16((mb / 32 + 2) * 4 + 32);
-        P.lay_col = P.lay_rp + (P.max_lpp_panels ? a16((P.max_lpp_panels + 1) * 4 + 32) : 0);
+        // records: panel records (lane-per-panel chunks) or 32 lane records
+        P.lay_col = P.lay_rp + a16(std::max<int64_t>(P.max_lpp_panels + 1, 32) * 4 + 32);
         P.lay_mask = P.lay_col + a16(mb * 4 + 32);
         P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
@@ -733,6 +778,28 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         SPC5_CUDA(cudaStreamSynchronize(st));
         dev_free(size16);
         dev_free(off16);
+    }
+    if (getenv("SPC5_PLAN_DEBUG")) {  // diagnostics: chunk modes and slot shape
+        std::vector<uint8_t> f((size_t)nc);
+        if (nc)
+            SPC5_CUDA(cudaMemcpy(f.data(), P.chunk_flags, (size_t)nc, cudaMemcpyDeviceToHost));
+        int64_t cnt[8] = {0};
+        for (uint8_t v : f) {
+            ++cnt[v & 7];
+        }
+        fprintf(stderr,
+                "spc5 plan: r=%d vs=%d nb=%lld np=%lld chunks=%lld target=%lld split_len=%lld "
+                "slot=%d B (rec@%lld col@%lld mask@%lld val@%lld) max_blocks=%lld max_values=%lld "
+                "max_lpp_panels=%lld split=%lld empty=%lld | flags: scan=%lld mid=%lld "
+                "empty=%lld lpr=%lld other=%lld\n",
+                m.r, m.vs, (long long)nb, (long long)np, (long long)nc,
+                (long long)P.chunk_target, (long long)P.split_len, P.slot_bytes,
+                (long long)P.lay_rp, (long long)P.lay_col, (long long)P.lay_mask,
+                (long long)P.lay_val, (long long)P.max_chunk_blocks,
+                (long long)P.max_chunk_values, (long long)P.max_lpp_panels,
+                (long long)P.num_split, (long long)P.num_empty, (long long)cnt[0],
+                (long long)(cnt[1] + cnt[3]), (long long)(cnt[2]), (long long)cnt[4],
+                (long long)(nc - cnt[0] - cnt[1] - cnt[3] - cnt[2] - cnt[4]));
     }
     P.built = true;
     return SPC5_OK;

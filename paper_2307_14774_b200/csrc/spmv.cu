@@ -289,6 +289,57 @@ __device__ __forceinline__ void row_dispatch(double &acc, uint32_t (&m)[U], int 
     }
 }
 
+// As row_slots / row_dispatch, but block k accumulates into acc[k] (the lane's
+// blocks of K different windows in lane-per-block mode).
+template <typename T, int U, int NS>
+__device__ __forceinline__ void row_slots_sep(double (&acc)[U], uint32_t (&m)[U], int (&h)[U],
+                                              const T *__restrict__ x,
+                                              const uint32_t (&col)[U],
+                                              const uint32_t (&vaddr)[U]) {
+    T xv[U][NS];
+    uint32_t vtop[U];
+    int h0[U];
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+        h0[k] = h[k];
+        vtop[k] = vaddr[k] + (uint32_t)(h[k] - 1) * (uint32_t)sizeof(T);
+        h[k] = max(h[k] - NS, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const uint32_t pos = bfind(m[k]);
+            m[k] &= ~(1u << pos);
+            xv[k][u] = ldg_pred(x + (col[k] + pos), u < h0[k]);
+        }
+    }
+#pragma unroll
+    for (int k = 0; k < U; ++k) {
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+            const T vv = lds_pred<T>(vtop[k] - (uint32_t)(u * sizeof(T)), u < h0[k]);
+            mac<T>(acc[k], vv, xv[k][u]);
+        }
+    }
+}
+template <typename T, int U>
+__device__ __forceinline__ void row_dispatch_sep(double (&acc)[U], uint32_t (&m)[U], int (&h)[U],
+                                                 const T *__restrict__ x,
+                                                 const uint32_t (&col)[U],
+                                                 const uint32_t (&vaddr)[U], int cmax) {
+    if (cmax <= 0) return;
+    if (cmax == 1) {
+        row_slots_sep<T, U, 1>(acc, m, h, x, col, vaddr);
+    } else if (cmax == 2) {
+        row_slots_sep<T, U, 2>(acc, m, h, x, col, vaddr);
+    } else if (cmax == 3) {
+        row_slots_sep<T, U, 3>(acc, m, h, x, col, vaddr);
+    } else {
+        for (int done = 0; done < cmax; done += 4) row_slots_sep<T, U, 4>(acc, m, h, x, col, vaddr);
+    }
+}
+
 
 
 // Lane 0 of the warp: copy one chunk into the slot at shared address `slot`
@@ -448,6 +499,294 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t p0, int npc
     }
 }
 
+// Lane-per-block mode: 32-block windows aligned to global block indices,
+// lane l owns block w+l (all R rows).  K windows per step: their metadata,
+// value offsets and x gathers are all issued before the first window's
+// segmented reduction, so K gathers per lane are in flight at once; the
+// windows are then reduced in order (carry chain).
+template <typename T, typename MT, int R, bool GENERIC, int K>
+__device__ __forceinline__ void lpb_chunk(const SpmvArgs &a, int64_t c, int64_t b0, int64_t p0,
+                                          int64_t pe, int n, int a0, int a1, bool head_mid,
+                                          bool slow, int sh0, uint32_t a_bits, uint32_t a_col,
+                                          uint32_t a_mask, uint32_t a_val, int lane,
+                                          const T *__restrict__ x, T *__restrict__ y) {
+    constexpr int MB = (int)sizeof(MT);
+    constexpr int LB = R * MB;
+    const unsigned lane_le = kFull >> (31 - lane);  // bits 0..lane
+    double carry[R];
+    bool carry_valid = false;
+    int carry_panel = 0;           // relative to p0
+    int pcur = head_mid ? 0 : -1;  // panel (rel. p0) of the block before the window
+    uint32_t vrel = 0;
+    for (int w0 = -sh0; w0 < a1; w0 += 32 * K) {
+        int pl[K];
+        unsigned hbits[K];
+        bool act[K];
+        uint32_t colk[K], vb[K];
+        LaneMasks<LB> mk[K];
+        // ---- metadata, value offsets and panels of the K windows
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int w = w0 + 32 * k;
+            const int br = w + lane;  // block relative to the chunk start
+            const bool counted = (unsigned)br < (unsigned)n;
+            act[k] = GENERIC ? (br >= a0 && br < a1) : counted;
+            const int bc = min(max(br, 0), n - 1);  // clamped: loads need no branch
+            colk[k] = lds_u32(a_col + (uint32_t)bc * 4u);
+            mk[k].load(a_mask + (uint32_t)bc * LB);
+            mk[k].clear_if(counted);
+            const int cnt = mk[k].popc();  // counted blocks advance the value cursor
+            const int incl = warp_incl_scan(cnt);
+            vb[k] = a_val + (vrel + (uint32_t)(incl - cnt)) * (uint32_t)sizeof(T);
+            vrel += (uint32_t)__shfl_sync(kFull, incl, 31);
+            pl[k] = 0;
+            hbits[k] = kFull;
+            if (w < a1) {
+                // panel starts in this window (first / last window: counted blocks only)
+                uint32_t W = lds_u32(a_bits + (uint32_t)((sh0 + w) >> 5) * 4u);
+                if (w < 0 || n - w < 32) {
+                    const int lo_i = max(-w, 0), hi_i = min(n - w, 32);
+                    W &= (hi_i >= 32 ? kFull : ((1u << hi_i) - 1u)) & ~((1u << lo_i) - 1u);
+                }
+                // lanes past the active range form their own segment (appending
+                // zero lanes to a panel's segment would change its association)
+                const unsigned sent = (a1 - w < 32) ? (1u << (a1 - w)) : 0u;
+                if (!slow) {
+                    pl[k] = pcur + __popc(W & lane_le);
+                    hbits[k] = W | sent | 1u;
+                    pcur += __popc(W);
+                } else {  // empty panels inside the chunk: search block_rowptr
+                    const int64_t bq = b0 + max(br, 0);
+                    int64_t lo = p0, hi = min(pe, a.num_panels - 1);
+                    while (lo < hi) {
+                        const int64_t mid = lo + (hi - lo + 1) / 2;
+                        if (__ldg(a.rowptr + mid) <= bq) lo = mid;
+                        else hi = mid - 1;
+                    }
+                    pl[k] = (int)(lo - p0);
+                    const int pprev = __shfl_up_sync(kFull, pl[k], 1);
+                    hbits[k] = __ballot_sync(kFull, lane > 0 && pl[k] != pprev) | sent | 1u;
+                }
+            }
+        }
+        // ---- products of every panel row of the lane's K blocks
+        double acc[R][K];
+#pragma unroll
+        for (int g = 0; g < R; ++g) {
+            uint32_t m[K], vr[K];
+            int h[K], cm = 0;
+#pragma unroll
+            for (int k = 0; k < K; ++k) {
+                const uint32_t mrow = mk[k].template row<MB>(g);
+                m[k] = act[k] ? mrow : 0u;
+                h[k] = __popc(m[k]);
+                cm = max(cm, h[k]);
+                vr[k] = vb[k];
+                vb[k] += (uint32_t)__popc(mrow) * (uint32_t)sizeof(T);
+                acc[g][k] = 0.0;
+            }
+            row_dispatch_sep<T, K>(acc[g], m, h, x, colk, vr, __reduce_max_sync(kFull, cm));
+        }
+        // ---- reduce the windows in order
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int w = w0 + 32 * k;
+            if (w >= a1) break;
+            const bool last = w + 32 >= a1;
+            double s[R];
+#pragma unroll
+            for (int g = 0; g < R; ++g) s[g] = acc[g][k];
+            // the panel carried from the previous window: add or flush
+            if (carry_valid) {
+                const bool continues = __shfl_sync(kFull, pl[k], 0) == carry_panel;
+                if (lane == 0) {
+                    if (continues) {
+#pragma unroll
+                        for (int g = 0; g < R; ++g) s[g] += carry[g];
+                    } else if (head_mid && carry_panel == 0) {
+#pragma unroll
+                        for (int g = 0; g < R; ++g) a.carry[c * R + g] = carry[g];
+                    } else {
+                        store_rows<T, R>(y, (p0 + carry_panel) * R, a.num_rows, carry,
+                                         a.accumulate);
+                    }
+                }
+                carry_valid = false;
+            }
+            // segmented scan over lanes of the same panel
+            const int segstart = 31 - __clz(hbits[k] & lane_le);
+#pragma unroll
+            for (int dd = 1; dd < 32; dd <<= 1) {
+                const bool take = lane - dd >= segstart;
+#pragma unroll
+                for (int g = 0; g < R; ++g) {
+                    const double t = __shfl_up_sync(kFull, s[g], dd);
+                    if (take) s[g] += t;
+                }
+            }
+            const bool tail = lane == 31 || ((hbits[k] >> (lane + 1)) & 1u);
+            // the window's last segment is carried unless the chunk ends here
+            if (tail && act[k] && (lane != 31 || last)) {
+                if (head_mid && pl[k] == 0) {
+#pragma unroll
+                    for (int g = 0; g < R; ++g) a.carry[c * R + g] = s[g];
+                } else {
+                    store_rows<T, R>(y, (p0 + pl[k]) * R, a.num_rows, s, a.accumulate);
+                }
+            }
+            if (last) break;
+#pragma unroll
+            for (int g = 0; g < R; ++g) carry[g] = __shfl_sync(kFull, s[g], 31);
+            carry_panel = __shfl_sync(kFull, pl[k], 31);
+            carry_valid = GENERIC ? __shfl_sync(kFull, act[k], 31) : true;
+        }
+    }
+}
+
+// Balanced-lane-range mode (scan chunks without empty panels): lane l owns
+// the contiguous blocks [l*n/32, (l+1)*n/32) of the chunk whatever the panel
+// lengths.  It walks them in order (U blocks per step, gathers first),
+// stores every panel that starts and ends inside its range, and keeps two
+// partials: F, the panel open from the left (closed inside the range), and L,
+// the panel open at the range end.  One segmented warp scan of L per chunk
+// joins panels that span lanes.  The plan's lane records give each lane's
+// first value and panel.  In range mode (GENERIC) the whole chunk is summed
+// the same way and only rows of panels in [p_lo, p_hi) are written, so the
+// result is bitwise the full product's.
+template <typename T, int R>
+__device__ __forceinline__ void blr_put(const SpmvArgs &a, int64_t c, int64_t p0, int p,
+                                        bool head_mid, const double *v, T *__restrict__ y,
+                                        bool generic) {
+    if (p == 0 && head_mid) {  // head of a split panel: carry slot, fixup adds it
+#pragma unroll
+        for (int g = 0; g < R; ++g) a.carry[c * R + g] = v[g];
+        return;
+    }
+    const int64_t P = p0 + p;
+    if (generic && (P < a.p_lo || P >= a.p_hi)) return;
+    store_rows<T, R>(y, P * R, a.num_rows, v, a.accumulate);
+}
+
+#ifndef SPC5_BLR
+#define SPC5_BLR 1
+#endif
+#ifndef SPC5_BLR_U
+#define SPC5_BLR_U (R <= 2 ? 4 : 2)
+#endif
+template <typename T, typename MT, int R, bool GENERIC, int U>
+__device__ __forceinline__ void blr_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int n,
+                                          bool head_mid, int sh0, uint32_t a_bits,
+                                          uint32_t a_lane, uint32_t a_col, uint32_t a_mask,
+                                          uint32_t a_val, int lane, const T *__restrict__ x,
+                                          T *__restrict__ y) {
+    constexpr int MB = (int)sizeof(MT);
+    constexpr int LB = R * MB;
+    const int sl = (lane * n) >> 5, el = ((lane + 1) * n) >> 5;
+    const bool nonempty = sl < el;
+    const uint32_t rec = lds_u32(a_lane + (uint32_t)lane * 4u);
+    uint32_t vaddr = a_val + (rec & 0xffffu) * (uint32_t)sizeof(T);
+    const int pf = (int)(rec >> 16);  // panel of the lane's first block
+    int p = pf;
+    auto start_bit = [&](int b) -> bool {
+        const uint32_t wrd = lds_u32(a_bits + (uint32_t)((sh0 + b) >> 5) * 4u);
+        return (wrd >> ((sh0 + b) & 31)) & 1u;
+    };
+    const bool first_start = nonempty && start_bit(sl);
+    const bool first_open = nonempty && !first_start;
+    double acc[R], F[R];
+#pragma unroll
+    for (int g = 0; g < R; ++g) acc[g] = F[g] = 0.0;
+    bool flushed = false;
+    const int my = el - sl;
+    const int maxlen = __reduce_max_sync(kFull, my);
+    for (int j = 0; j < maxlen; j += U) {
+        uint32_t col[U], vbk[U];
+        LaneMasks<LB> mk[U];
+        bool st[U];
+        uint32_t vnext = vaddr;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            const bool ok = j + k < my;
+            const int b = ok ? sl + j + k : 0;
+            col[k] = lds_u32(a_col + (uint32_t)b * 4u);
+            mk[k].load(a_mask + (uint32_t)b * LB);
+            mk[k].clear_if(ok);
+            st[k] = ok && j + k > 0 && start_bit(b);
+            vbk[k] = vnext;
+            vnext += (uint32_t)mk[k].popc() * (uint32_t)sizeof(T);
+        }
+        vaddr = vnext;
+        // gathers of all U blocks (every row), then the blocks in order
+        double part[U][R];
+#pragma unroll
+        for (int g = 0; g < R; ++g) {
+            uint32_t m[U], vr[U];
+            int h[U], cm = 0;
+            double pg[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                m[k] = mk[k].template row<MB>(g);
+                h[k] = __popc(m[k]);
+                cm = max(cm, h[k]);
+                vr[k] = vbk[k];
+                vbk[k] += (uint32_t)h[k] * (uint32_t)sizeof(T);
+                pg[k] = 0.0;
+            }
+            row_dispatch_sep<T, U>(pg, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
+#pragma unroll
+            for (int k = 0; k < U; ++k) part[k][g] = pg[k];
+        }
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            if (st[k]) {  // block starts a new panel: close the current one
+                if (!flushed && first_open) {
+#pragma unroll
+                    for (int g = 0; g < R; ++g) F[g] = acc[g];
+                } else {
+                    blr_put<T, R>(a, c, p0, p, head_mid, acc, y, GENERIC);
+                }
+                flushed = true;
+                ++p;
+#pragma unroll
+                for (int g = 0; g < R; ++g) acc[g] = 0.0;
+            }
+#pragma unroll
+            for (int g = 0; g < R; ++g) acc[g] += part[k][g];
+        }
+    }
+    // join the panels that span lanes: segmented inclusive scan of L = acc
+    const bool seg = first_start || flushed;
+    const unsigned segs = __ballot_sync(kFull, seg) | 1u;
+    const unsigned lane_le = kFull >> (31 - lane);
+    const int segstart = 31 - __clz(segs & lane_le);
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const bool take = lane - dd >= segstart;
+#pragma unroll
+        for (int g = 0; g < R; ++g) {
+            const double t = __shfl_up_sync(kFull, acc[g], dd);
+            if (take) acc[g] += t;
+        }
+    }
+    double prev[R];
+#pragma unroll
+    for (int g = 0; g < R; ++g) {
+        prev[g] = __shfl_up_sync(kFull, acc[g], 1);
+        if (lane == 0) prev[g] = 0.0;
+    }
+    if (nonempty) {
+        if (first_open && flushed) {  // the panel open from the left ends here
+            double v[R];
+#pragma unroll
+            for (int g = 0; g < R; ++g) v[g] = prev[g] + F[g];
+            blr_put<T, R>(a, c, p0, pf, head_mid, v, y, GENERIC);
+        } else if (first_start && sl > 0) {  // it ended at this lane's boundary
+            blr_put<T, R>(a, c, p0, pf - 1, head_mid, prev, y, GENERIC);
+        }
+        if (lane == 31) blr_put<T, R>(a, c, p0, p, head_mid, acc, y, GENERIC);
+    }
+}
+
 // K2.  Each warp takes chunks c_lo + (blockIdx.x + k*gridDim.x)*W + warp,
 // k = 0, 1, ...; the CTA's warps work on neighbouring chunks (x reuse in L1).
 // GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
@@ -464,7 +803,6 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
     extern __shared__ __align__(128) uint8_t smem[];
     const int lane = threadIdx.x & 31;
     const int warp = threadIdx.x >> 5;
-    const unsigned lane_le = kFull >> (31 - lane);  // bits 0..lane
     const T *__restrict__ x = static_cast<const T *>(a.x);
     T *__restrict__ y = static_cast<T *>(a.y);
 
@@ -520,14 +858,6 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
         const int64_t pe = lds_s64(sbase + 32);
         const int flags = (int)lds_u32(sbase + 40);
         const uint32_t rec_off = lds_u32(sbase + 44);
-#ifdef SPC5_K2_STREAM_ONLY  // experiment: stream the matrix, skip the products
-        if (b1 >= b0) {
-            if (b1 > b0 + 1000000) y[0] = (T)v0;
-        }
-#else
-        if (false) {}
-#endif
-        else {
         const bool head_mid = flags & 1;  // first block continues a panel of earlier chunks
         const bool slow = flags & 2;      // empty panels inside: search block_rowptr
         const int n = (int)(b1 - b0);
@@ -544,119 +874,16 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
         const uint32_t a_val = sbase + a.lay_val + (uint32_t)((v0 * (int64_t)sizeof(T)) & 15);
         const int sh0 = (int)((b0 + a.off32) & 31);
 
-        double carry[R];
-        bool carry_valid = false;
-        int carry_panel = 0;           // relative to p0
-        int pcur = head_mid ? 0 : -1;  // panel (rel. p0) of the block before the window
-        uint32_t vrel = 0;
-
         if (flags & 4) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, p0, (int)(pe - p0), (flags >> 3) & 3, a_rp, a_col,
                                          a_mask, a_val, lane, x, y);
-        } else
-        for (int w = -sh0; w < a1; w += 32) {
-            const bool last = w + 32 >= a1;
-            const int br = w + lane;  // block relative to the chunk start
-            const bool counted = (unsigned)br < (unsigned)n;
-            const bool act = GENERIC ? (br >= a0 && br < a1) : counted;
-            const int bc = min(max(br, 0), n - 1);  // clamped: loads need no branch
-            const uint32_t col = lds_u32(a_col + (uint32_t)bc * 4u);
-            LaneMasks<LB> mk;
-            mk.load(a_mask + (uint32_t)bc * LB);
-            mk.clear_if(counted);
-            const int cnt = mk.popc();  // counted blocks advance the value cursor
-            const int incl = warp_incl_scan(cnt);
-            const int total = __shfl_sync(kFull, incl, 31);
-            // ---- panel starts in this window
-            uint32_t W = lds_u32(a_bits + (uint32_t)((sh0 + w) >> 5) * 4u);
-            if (w < 0 || n - w < 32) {  // first / last window: counted blocks only
-                const int lo_i = max(-w, 0), hi_i = min(n - w, 32);
-                W &= (hi_i >= 32 ? kFull : ((1u << hi_i) - 1u)) & ~((1u << lo_i) - 1u);
-            }
-            // lanes past the active range form their own segment (appending zero
-            // lanes to a panel's segment would change the association of its sum)
-            const unsigned sent = (a1 - w < 32) ? (1u << (a1 - w)) : 0u;
-            int pl;  // panel relative to p0
-            unsigned hbits;
-            if (!slow) {
-                pl = pcur + __popc(W & lane_le);
-                hbits = W | sent | 1u;
-                pcur += __popc(W);
-            } else {  // empty panels inside the chunk: search block_rowptr
-                const int64_t bq = b0 + max(br, 0);
-                int64_t lo = p0, hi = min(pe, a.num_panels - 1);
-                while (lo < hi) {
-                    const int64_t mid = lo + (hi - lo + 1) / 2;
-                    if (__ldg(a.rowptr + mid) <= bq) lo = mid;
-                    else hi = mid - 1;
-                }
-                pl = (int)(lo - p0);
-                const int pprev = __shfl_up_sync(kFull, pl, 1);
-                hbits = __ballot_sync(kFull, lane > 0 && pl != pprev) | sent | 1u;
-            }
-
-            // ---- products: each panel row of the lane's block
-            double acc[R];
-            const uint32_t col1[1] = {col};
-            uint32_t vaddr = a_val + (vrel + (uint32_t)(incl - cnt)) * (uint32_t)sizeof(T);
-#pragma unroll
-            for (int g = 0; g < R; ++g) {
-                const uint32_t mrow = mk.template row<MB>(g);
-                uint32_t m1[1] = {act ? mrow : 0u};
-                int h1[1] = {__popc(m1[0])};
-                const uint32_t v1[1] = {vaddr};
-                acc[g] = 0.0;
-                row_dispatch<T, 1>(acc[g], m1, h1, x, col1, v1, __reduce_max_sync(kFull, h1[0]));
-                vaddr += (uint32_t)__popc(mrow) * (uint32_t)sizeof(T);
-            }
-            vrel += (uint32_t)total;
-
-            // ---- the panel carried from the previous window: add or flush
-            if (carry_valid) {
-                const bool continues = __shfl_sync(kFull, pl, 0) == carry_panel;
-                if (lane == 0) {
-                    if (continues) {
-#pragma unroll
-                        for (int g = 0; g < R; ++g) acc[g] += carry[g];
-                    } else if (head_mid && carry_panel == 0) {
-#pragma unroll
-                        for (int g = 0; g < R; ++g) a.carry[c * R + g] = carry[g];
-                    } else {
-                        store_rows<T, R>(y, (p0 + carry_panel) * R, a.num_rows, carry,
-                                         a.accumulate);
-                    }
-                }
-                carry_valid = false;
-            }
-
-            // ---- segmented scan over lanes of the same panel
-            const int segstart = 31 - __clz(hbits & lane_le);
-#pragma unroll
-            for (int dd = 1; dd < 32; dd <<= 1) {
-                const bool take = lane - dd >= segstart;
-#pragma unroll
-                for (int g = 0; g < R; ++g) {
-                    const double t = __shfl_up_sync(kFull, acc[g], dd);
-                    if (take) acc[g] += t;
-                }
-            }
-            const bool tail = lane == 31 || ((hbits >> (lane + 1)) & 1u);
-            // the window's last segment is carried unless the chunk ends here
-            if (tail && act && (lane != 31 || last)) {
-                if (head_mid && pl == 0) {
-#pragma unroll
-                    for (int g = 0; g < R; ++g) a.carry[c * R + g] = acc[g];
-                } else {
-                    store_rows<T, R>(y, (p0 + pl) * R, a.num_rows, acc, a.accumulate);
-                }
-            }
-            if (last) break;
-#pragma unroll
-            for (int g = 0; g < R; ++g) carry[g] = __shfl_sync(kFull, acc[g], 31);
-            carry_panel = __shfl_sync(kFull, pl, 31);
-            carry_valid = GENERIC ? __shfl_sync(kFull, act, 31) : true;
-        }
-
+        } else if (!slow && SPC5_BLR) {  // balanced lane ranges
+            blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, a_bits,
+                                                           a_rp, a_col, a_mask, a_val, lane, x, y);
+        } else {
+            constexpr int KW = R <= 2 ? 4 : (R == 4 ? 2 : 1);  // windows per step
+            lpb_chunk<T, MT, R, GENERIC, KW>(a, c, b0, p0, pe, n, a0, a1, head_mid, slow, sh0,
+                                             a_bits, a_col, a_mask, a_val, lane, x, y);
         }
         // ---- release the slot and refill it with the chunk S ahead
         __syncwarp();

@@ -3,9 +3,13 @@
 No public matrix suite is used (SuiteSparse is absent offline); these
 generators stand in with the shapes, sizes and value distributions that
 BASELINE.json names.  Host versions (numpy) live here; the device versions
-(``spc5_gen_stencil27`` in csrc/gen.cu) produce bit-identical CSR arrays so a
-row slice generated on the host checks a slice of a device-generated matrix
-(the sliced oracle).
+(``spc5_gen_stencil27_*``, ``spc5_gen_powerlaw_*``, ``spc5_gen_fem_*`` in
+csrc/aux.cu) produce bit-identical CSR arrays so a row slice generated on the
+host checks a slice of a device-generated matrix (the sliced oracle, SURVEY.md
+8(c)).  Column sampling is stratified with integer arithmetic only (distinct
+and sorted by construction, no transcendental functions on either side), and
+the lognormal row lengths of config 3 come from a quantile table made here
+once and handed to the device.
 
 Values are position keyed, ``v(i, j) = 2*u(i, j) - 1`` with
 ``u = (splitmix64((i << 32) ^ j ^ seedmix) >> 11) * 2**-53`` -- the scheme the
@@ -86,13 +90,116 @@ def config1(seed: int = MATRIX_SEED) -> CsrMatrix:
     return make_random(8192, 8192, 16, 0.0, seed, "f64")
 
 
+# ---------------------------------------------------------------- config 3
+PL_N = 4_194_304
+PL_WINDOW = 4096
+PL_TABLE_BITS = 12
+PL_SALT = np.uint64(0x5BD1E995)
+
+
+def powerlaw_len_table(bits: int = PL_TABLE_BITS, mean: float = 16.0, sigma: float = 1.5,
+                       max_len: int = 8192) -> np.ndarray:
+    """Row lengths: 2^bits quantiles of lognormal(mean, sigma), rounded, clipped to [1, max_len]."""
+    from scipy.special import ndtri
+    k = 1 << bits
+    q = (np.arange(k, dtype=np.float64) + 0.5) / k
+    mu = np.log(mean) - sigma * sigma / 2.0
+    return np.clip(np.rint(np.exp(mu + sigma * ndtri(q))), 1, max_len).astype(np.int32)
+
+
+def _pl_key(seedmix, i: int, s, tag: int) -> np.ndarray:
+    s = np.asarray(s, dtype=np.uint64)
+    return mix64(seedmix ^ (np.uint64(i) << np.uint64(24)) ^ (s << np.uint64(2)) ^ np.uint64(tag))
+
+
+def _strata(lo: int, width: int, k: int, key: np.ndarray) -> np.ndarray:
+    s = np.arange(k, dtype=np.int64)
+    a = lo + s * width // k
+    b = lo + (s + 1) * width // k
+    return a + (key % (b - a).astype(np.uint64)).astype(np.int64)
+
+
+def powerlaw_rows(lo: int, hi: int, n: int = PL_N, precision: str = "f32",
+                  seed: int = MATRIX_SEED, table: np.ndarray | None = None) -> CsrMatrix:
+    """Rows [lo, hi) of the config-3 power-law matrix (twin of csrc/aux.cu powerlaw_*).
+
+    Row i: length from the quantile table, 80 % of the columns stratified over
+    i +- 4096, the rest stratified over [0, n), merged without duplicates;
+    values U(-1, 1) keyed by (i, j).
+    """
+    table = powerlaw_len_table() if table is None else table
+    bits = int(np.log2(len(table)))
+    seedmix = seed_mix(seed) ^ PL_SALT
+    cols, ptr = [], [0]
+    for i in range(lo, hi):
+        ln = int(table[int(_pl_key(seedmix, i, 0, 0)) >> (64 - bits)])
+        lo_w, hi_w = max(0, i - PL_WINDOW), min(n - 1, i + PL_WINDOW)
+        w = hi_w - lo_w + 1
+        k_loc = min((4 * ln + 2) // 5, w)
+        k_uni = min(ln - k_loc, n)
+        loc = _strata(lo_w, w, k_loc, _pl_key(seedmix, i, np.arange(k_loc), 1))
+        uni = _strata(0, n, k_uni, _pl_key(seedmix, i, np.arange(k_uni), 2))
+        c = np.union1d(loc, uni)
+        cols.append(c)
+        ptr.append(ptr[-1] + len(c))
+    col = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+    row_ptr = np.asarray(ptr, dtype=np.int64)
+    rows = np.repeat(np.arange(lo, hi, dtype=np.int64), np.diff(row_ptr))
+    vals = keyed_uniform(rows, col, seed).astype(dtype_for(precision))
+    return CsrMatrix(hi - lo, n, row_ptr, col.astype(np.int32), vals)
+
+
+# ---------------------------------------------------------------- config 4
+FEM_NODES = 262_144
+FEM_WINDOW = 2048
+FEM_NBR = 26
+SQRT3 = 1.7320508075688772
+
+
+def fem_neighbours(q: int, nodes: int = FEM_NODES, seed: int = MATRIX_SEED) -> np.ndarray:
+    """The 26 nodes coupled to node q: stratified over q +- 2048, q excluded, ascending."""
+    lo_w = max(0, q - FEM_WINDOW)
+    w = min(nodes - 1, q + FEM_WINDOW) - lo_w
+    p = _strata(lo_w, w, FEM_NBR, _pl_key(seed_mix(seed) ^ PL_SALT, q, np.arange(FEM_NBR), 3))
+    return np.where(p >= q, p + 1, p)
+
+
+def fem_rows(lo: int, hi: int, nodes: int = FEM_NODES, precision: str = "f64",
+             seed: int = MATRIX_SEED) -> CsrMatrix:
+    """Rows [lo, hi) of the config-4 FEM-like matrix (twin of csrc/aux.cu fem_*).
+
+    Row 3q+d holds the dense 3x3 blocks of node q and its 26 neighbours
+    (81 entries); values sqrt(3) * (u1 + u2 + u3 + u4 - 2), u_k chained
+    splitmix64 uniforms keyed by (row, col).
+    """
+    cols = []
+    for i in range(lo, hi):
+        q = i // 3
+        nodes_q = np.union1d(fem_neighbours(q, nodes, seed), [q])
+        cols.append((3 * nodes_q[:, None] + np.arange(3)[None, :]).ravel())
+    col = np.concatenate(cols) if cols else np.zeros(0, np.int64)
+    row_ptr = np.arange(hi - lo + 1, dtype=np.int64) * 3 * (FEM_NBR + 1)
+    rows = np.repeat(np.arange(lo, hi, dtype=np.int64), 3 * (FEM_NBR + 1))
+    key = (rows.astype(np.uint64) << np.uint64(32)) ^ col.astype(np.uint64) ^ seed_mix(seed)
+    h = mix64(key)
+    acc = np.zeros(len(col), dtype=np.float64)
+    with np.errstate(over="ignore"):
+        for _ in range(4):
+            acc += (h >> np.uint64(11)).astype(np.float64) * 2.0 ** -53
+            h = mix64(h + GOLDEN)
+    vals = ((acc - 2.0) * SQRT3).astype(dtype_for(precision))
+    return CsrMatrix(hi - lo, 3 * nodes, row_ptr, col.astype(np.int32), vals)
+
+
 # Config descriptors used by bench.py and the tests.  ``formats`` are (r, vs).
 CONFIGS = {
     1: dict(name="random8192_16perrow_f64", precision="f64", formats=[(1, 8)]),
     2: dict(name="stencil27_128cubed_f64", precision="f64", n=128,
             formats=[(1, 8), (2, 8), (4, 8), (8, 8)]),
-    3: dict(name="powerlaw_4M_f32", precision="f32", formats=[(1, 16), (2, 16), (4, 16)]),
-    4: dict(name="fem_786K_f64", precision="f64", formats=[(4, 8), (8, 8)]),
+    3: dict(name="powerlaw_4M_f32", precision="f32", gen="powerlaw", rows=PL_N, cols=PL_N,
+            formats=[(1, 16), (2, 16), (4, 16)]),
+    4: dict(name="fem_786K_f64", precision="f64", gen="fem", rows=3 * FEM_NODES,
+            cols=3 * FEM_NODES, formats=[(4, 8), (8, 8)]),
     5: dict(name="stencil27_400cubed", precision="f64", n=400,
             formats=[(1, 8), (2, 8), (4, 8), (8, 8)]),
 }

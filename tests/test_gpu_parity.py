@@ -123,6 +123,19 @@ def test_spmv_small_vs_oracle(spc5, name):
             assert spc5.partition_by_nnz(s, int(w)).ranges == [tuple(t) for t in ranges]
 
 
+@pytest.mark.parametrize("name", ["longrows", "longrows_f32", "tall", "rand05", "rand17"])
+def test_spmv_repeatable_bitwise(spc5, name):
+    """Every format: repeated products are bitwise identical (catches races on
+    y rows and carry slots between lanes, warps and chunks)."""
+    m = small_case(name)
+    x = case_x(name, m)
+    for r, vs, _ in fmt_keys(expected_small()["cases"][name]):
+        s = spc5.csr_to_spc5(m, r, vs)
+        y0 = spc5.spmv(s, x)
+        for _ in range(6):
+            assert spc5.spmv(s, x).tobytes() == y0.tobytes(), (name, r, vs)
+
+
 def test_identity_exact_and_cancellation(spc5):
     m = small_case("identity32")
     x = np.random.default_rng(3).uniform(-1, 1, 32)
@@ -391,3 +404,88 @@ def test_config2_full_size(spc5):
         assert float(err.max()) <= 1e-12, (r, float(err.max()))
         del s
         torch.cuda.empty_cache()
+
+
+# ---------------------------------------------------------------- configs 3 and 4
+def _device_rows(gen, lo, hi, prec):
+    """Rows [lo, hi) of config 3 ('powerlaw') or 4 ('fem') from the device generator."""
+    import torch
+    from paper_2307_14774_b200 import _native as nat
+    from paper_2307_14774_b200.workloads import FEM_NODES, PL_N, PL_TABLE_BITS, powerlaw_len_table
+    tdt = torch.float64 if prec == "f64" else torch.float32
+    pc = 1 if prec == "f64" else 0
+    rp = torch.empty(hi - lo + 1, dtype=torch.int64, device="cuda")
+    table = torch.from_numpy(powerlaw_len_table()).to("cuda")
+    if gen == "powerlaw":
+        nat.check(nat.lib.spc5_gen_powerlaw_rowptr(PL_N, lo, hi, 0, table.data_ptr(),
+                                                   PL_TABLE_BITS, rp.data_ptr(), 0))
+    else:
+        nat.check(nat.lib.spc5_gen_fem_rowptr(FEM_NODES, lo, hi, rp.data_ptr(), 0))
+    nnz = int(rp[-1])
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
+    va = torch.empty(max(nnz, 1), dtype=tdt, device="cuda")
+    if gen == "powerlaw":
+        nat.check(nat.lib.spc5_gen_powerlaw_fill(PL_N, lo, hi, pc, 0, table.data_ptr(),
+                                                 PL_TABLE_BITS, rp.data_ptr(), ci.data_ptr(),
+                                                 va.data_ptr(), 0))
+    else:
+        nat.check(nat.lib.spc5_gen_fem_fill(FEM_NODES, lo, hi, pc, 0, rp.data_ptr(),
+                                            ci.data_ptr(), va.data_ptr(), 0))
+    torch.cuda.synchronize()
+    return rp, ci[:nnz], va[:nnz]
+
+
+@pytest.mark.parametrize("gen,prec,lo,hi", [
+    ("powerlaw", "f32", 0, 3000), ("powerlaw", "f32", 2_000_000, 2_001_500),
+    ("powerlaw", "f32", 4_194_304 - 1500, 4_194_304), ("powerlaw", "f64", 777, 1777),
+    ("fem", "f64", 0, 1500), ("fem", "f64", 400_000, 401_000),
+    ("fem", "f64", 786_432 - 1200, 786_432), ("fem", "f32", 12_345, 13_345)])
+def test_config34_device_generator_matches_host(spc5, gen, prec, lo, hi):
+    from paper_2307_14774_b200.workloads import fem_rows, powerlaw_rows
+    host = (powerlaw_rows if gen == "powerlaw" else fem_rows)(lo, hi, precision=prec)
+    rp, ci, va = _device_rows(gen, lo, hi, prec)
+    assert np.array_equal(rp.cpu().numpy(), host.row_ptr)
+    assert np.array_equal(ci.cpu().numpy(), host.col_idx)
+    assert va.cpu().numpy().tobytes() == host.values.tobytes()
+
+
+def _full_config_parity(spc5, cfg_id):
+    """A BASELINE config at full size: device-generated CSR, every format's
+    conversion bit-exact against the oracle, y within tolerance of the oracle
+    scalar path and inside the VERIFY_FACTOR budget of the exact sums."""
+    import torch
+    from paper_2307_14774_b200.mmio import CsrMatrix
+    from paper_2307_14774_b200.workloads import CONFIGS, x_vector
+    cfg = CONFIGS[cfg_id]
+    prec = cfg["precision"]
+    rp, ci, va = _device_rows(cfg["gen"], 0, cfg["rows"], prec)
+    m = CsrMatrix(cfg["rows"], cfg["cols"], rp.cpu().numpy(), ci.cpu().numpy(), va.cpu().numpy())
+    del rp, ci, va
+    x = x_vector(m.num_cols, prec)
+    _, abs_ref = oracle.csr_reference(m, x)
+    for r, vs in cfg["formats"]:
+        ref = oracle.csr_to_spc5(m, r, vs)
+        s = spc5.csr_to_spc5(m, r, vs)
+        for f in ("block_rowptr", "block_colidx", "block_masks", "values"):
+            assert np.array_equal(getattr(s, f), getattr(ref, f)), (r, vs, f)
+        y = spc5.spmv(s, x)
+        y_ref = np.zeros(m.num_rows, dtype=x.dtype)
+        oracle.spmv_spc5_scalar(ref, x, y_ref, threads=oracle.threads())
+        err = oracle.relative_error(y, y_ref, abs_ref)
+        assert float(err.max()) <= TOL[prec], (r, vs, float(err.max()))
+        scaled = oracle.scaled_error(m, y, x)
+        assert float(scaled.max()) <= oracle.VERIFY_FACTOR, (r, vs)
+        del s
+        torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_config3_full_size(spc5):
+    """BASELINE config 3: power-law 4,194,304^2, f32, beta(1|2|4, 16)."""
+    _full_config_parity(spc5, 3)
+
+
+@pytest.mark.slow
+def test_config4_full_size(spc5):
+    """BASELINE config 4: FEM-like 786,432^2 with dense 3x3 blocks, f64, beta(4|8, 8)."""
+    _full_config_parity(spc5, 4)
