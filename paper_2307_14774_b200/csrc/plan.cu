@@ -225,16 +225,18 @@ __global__ void pstart_bits_kernel(int64_t np, const int64_t *__restrict__ rowpt
 }
 
 // per chunk: bit0 = first block is not a panel start, bit1 = empty panels
-// inside, bit2 = lane-per-panel-row mode (whole, non-empty panels of similar
+// inside, bit2 = lane-per-panel-row mode (non-empty panels of similar
 // length, >= kLppMinLanes lanes busy), bits3-4 = log2 G: in that mode each
 // panel row is split over G lanes (contiguous block ranges, partial sums
-// combined by a butterfly), so short chunks still fill the warp
+// combined by a butterfly), so short chunks still fill the warp; bit5 = in
+// that mode, the last panel continues into the next chunk
 constexpr int64_t kLppMinLanes = 24;  // panels * r * G
 __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                                    const int64_t *__restrict__ chunk_b,
                                    const int64_t *__restrict__ chunk_p,
                                    const int64_t *__restrict__ rowptr,
-                                   const int64_t *__restrict__ empty, int64_t ne, uint8_t *flags) {
+                                   const int64_t *__restrict__ empty, int64_t ne, int lpr_split,
+                                   uint8_t *flags) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     uint8_t f = rowptr[chunk_p[c]] < chunk_b[c] ? 1 : 0;
@@ -247,18 +249,24 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
         else hi = mid;
     }
     if (lo < ne && empty[lo] < hi_p) f |= 2;
-    if (!(f & 3)) {
+    if (!(f & 2)) {
+        // lane-per-panel-row candidate: the chunk's panels, the first possibly
+        // started in an earlier chunk (bit0, carry slot) and the last possibly
+        // continuing into the next one (bit5)
         const int64_t cb0 = chunk_b[c], cb1 = chunk_b[c + 1];
         const bool ends_clean = hi_p >= np ? cb1 == nb : rowptr[hi_p] == cb1;
-        const int64_t npc = hi_p - lo_p;
-        if (ends_clean && npc > 0 && npc * r <= 32 * 64) {
+        const int64_t npc = hi_p - lo_p + (ends_clean ? 0 : 1);
+        // split pieces of long panels run faster in balanced-lane-range mode
+        const bool whole = !(f & 1) && ends_clean;
+        if ((whole || lpr_split) && npc > 0 && npc * r <= 32 * 64) {
             int64_t maxlen = 0;
-            for (int64_t p = lo_p; p < hi_p; ++p) maxlen = max(maxlen, rowptr[p + 1] - rowptr[p]);
+            for (int64_t p = lo_p; p < lo_p + npc; ++p)
+                maxlen = max(maxlen, min(rowptr[p + 1], cb1) - max(rowptr[p], cb0));
             int lg = 0;  // G = 1 << lg lanes per panel row, each with >= 1 block
             while (lg < 3 && npc * r * (2 << lg) <= 32 && maxlen >= (2 << lg)) ++lg;
             if (npc * r * (1 << lg) >= kLppMinLanes && maxlen <= 64 * (1 << lg) &&
                 maxlen * npc <= 2 * (cb1 - cb0) + 4 * npc)
-                f |= 4 | (lg << 3);
+                f |= 4 | (lg << 3) | (ends_clean ? 0 : 32);
         }
     }
     flags[c] = f;
@@ -284,7 +292,8 @@ __global__ void blob_size_kernel(int64_t nc, const int64_t *__restrict__ chunk_b
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     int64_t nw, nr;
-    blob_shape(chunk_b[c], chunk_b[c + 1], chunk_p[c + 1] - chunk_p[c], flags[c], off32, &nw, &nr);
+    blob_shape(chunk_b[c], chunk_b[c + 1], chunk_p[c + 1] - chunk_p[c] + ((flags[c] >> 5) & 1),
+               flags[c], off32, &nw, &nr);
     size16[c] = (64 + a16_dev(nw * 4) + a16_dev(nr * 4)) / 16;
 }
 
@@ -303,8 +312,9 @@ __global__ void blob_fill_kernel(int64_t nc, int r, int vs, int off32,
     for (int64_t c = warp; c < nc; c += nwarps) {
         const int64_t b0 = chunk_b[c], b1 = chunk_b[c + 1], p0 = chunk_p[c], pe = chunk_p[c + 1];
         const int f = flags[c];
+        const int64_t npc = pe - p0 + ((f >> 5) & 1);  // lane-per-panel: incl. a tail panel
         int64_t nw, nr;
-        blob_shape(b0, b1, pe - p0, f, off32, &nw, &nr);
+        blob_shape(b0, b1, npc, f, off32, &nw, &nr);
         uint8_t *bl = blob + (c ? off16_incl[c - 1] : 0) * 16;
         const int rec_off = (int)(64 + a16_dev(nw * 4));
         if (lane == 0) {
@@ -313,7 +323,7 @@ __global__ void blob_fill_kernel(int64_t nc, int r, int vs, int off32,
             h[1] = b1;
             h[2] = chunk_v[c];
             h[3] = p0;
-            h[4] = pe;
+            h[4] = (f & 4) ? p0 + npc : pe;
             reinterpret_cast<int *>(bl)[10] = f;
             reinterpret_cast<int *>(bl)[11] = rec_off;
             h[6] = h[7] = 0;
@@ -355,11 +365,14 @@ __global__ void blob_fill_kernel(int64_t nc, int r, int vs, int off32,
         uint32_t running = 0;
         for (int64_t q0 = 0; q0 < nr; q0 += 32) {
             const int64_t q = q0 + lane;
-            const int64_t s = q < nr ? rowptr[p0 + q] - b0 : 0;
+            // panel p0+q's blocks inside the chunk: [max(rowptr, b0), min(rowptr', b1))
+            const int64_t s = q < nr ? min(max(rowptr[p0 + q], b0), b1) - b0 : 0;
             int cnt = 0;
-            if (q < nr - 1)
-                for (int64_t b = rowptr[p0 + q]; b < rowptr[p0 + q + 1]; ++b)
+            if (q < nr - 1) {
+                const int64_t e = min(rowptr[p0 + q + 1], b1);
+                for (int64_t b = b0 + s; b < e; ++b)
                     for (int rr = 0; rr < r; ++rr) cnt += __popc(load_mask(masks, b * r + rr, vs));
+            }
             int incl = cnt;
             for (int d = 1; d < 32; d <<= 1) {
                 const int t = __shfl_up_sync(0xffffffffu, incl, d);
@@ -400,7 +413,8 @@ __global__ void issue_rec_kernel(int64_t nc, int lb, int vb, const int64_t *__re
 __global__ void lpp_panels_kernel(int64_t nc, const int64_t *__restrict__ chunk_p,
                                   const uint8_t *__restrict__ flags, unsigned long long *out) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (c < nc && (flags[c] & 4)) atomicMax(out, (unsigned long long)(chunk_p[c + 1] - chunk_p[c]));
+    if (c < nc && (flags[c] & 4))
+        atomicMax(out, (unsigned long long)(chunk_p[c + 1] - chunk_p[c] + ((flags[c] >> 5) & 1)));
 }
 
 __global__ void narrow_kernel(const int64_t *in, int64_t n, int *out) {
@@ -683,9 +697,11 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         unsigned long long *d_mx = nullptr;
         SPC5_TRY(dev_alloc(&d_mx, 1));
         const int64_t per_block = 4 + m.r * m.mask_bytes();
+        int64_t win_cap = 6 * 1024;  // bytes of the fullest split window (knob SPC5_WIN_KB)
+        if (const char *e = getenv("SPC5_WIN_KB")) win_cap = std::max(1, atoi(e)) * 1024;
         int64_t sl = 512;
         for (; sl > 1; sl >>= 1) {
-            if (sl * per_block > 6 * 1024) continue;
+            if (sl * per_block > win_cap) continue;
             unsigned long long h_mx = 0;
             SPC5_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));
             window_values_max_kernel<<<(unsigned)std::min<int64_t>(cdiv(cdiv(nb, sl) + 1, 8),
@@ -695,7 +711,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
             SPC5_CUDA(cudaGetLastError());
             SPC5_CUDA(cudaMemcpyAsync(&h_mx, d_mx, sizeof(h_mx), cudaMemcpyDeviceToHost, st));
             SPC5_CUDA(cudaStreamSynchronize(st));
-            if (sl * per_block + (int64_t)h_mx * m.value_bytes() <= 6 * 1024) break;
+            if (sl * per_block + (int64_t)h_mx * m.value_bytes() <= win_cap) break;
         }
         dev_free(d_mx);
         P.split_len = sl;
@@ -707,7 +723,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
-            P.num_empty, P.chunk_flags);
+            P.num_empty, getenv("SPC5_LPR_SPLIT") ? 1 : 0, P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
         unsigned long long *d_st = nullptr, h_st[3] = {0, 0, 0};
         SPC5_TRY(dev_alloc(&d_st, 3));

@@ -437,8 +437,8 @@ __device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s
 }
 
 template <typename T, typename MT, int R, bool GENERIC>
-__device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t p0, int npc, int lg,
-                                          uint32_t a_rec, uint32_t a_col, uint32_t a_mask,
+__device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int npc,
+                                          int lg, bool head_mid, uint32_t a_rec, uint32_t a_col, uint32_t a_mask,
                                           uint32_t a_val, int lane, const T *__restrict__ x,
                                           T *__restrict__ y) {
     constexpr int MB = (int)sizeof(MT);
@@ -492,9 +492,13 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t p0, int npc
         for (int o = 1; o < G; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
         const int64_t p = p0 + q;
         const int64_t row = p * R + rr;
-        if (sub == 0 && pv && row < a.num_rows && (!GENERIC || (p >= a.p_lo && p < a.p_hi))) {
-            const T sv = (T)acc;
-            y[row] = a.accumulate ? y[row] + sv : sv;
+        if (sub == 0 && pv) {
+            if (q == 0 && head_mid) {  // head of a split panel: carry slot, fixup adds it
+                a.carry[c * R + rr] = acc;
+            } else if (row < a.num_rows && (!GENERIC || (p >= a.p_lo && p < a.p_hi))) {
+                const T sv = (T)acc;
+                y[row] = a.accumulate ? y[row] + sv : sv;
+            }
         }
     }
 }
@@ -875,8 +879,8 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
         const int sh0 = (int)((b0 + a.off32) & 31);
 
         if (flags & 4) {  // lane-per-panel chunk
-            lpp_chunk<T, MT, R, GENERIC>(a, p0, (int)(pe - p0), (flags >> 3) & 3, a_rp, a_col,
-                                         a_mask, a_val, lane, x, y);
+            lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
+                                         a_rp, a_col, a_mask, a_val, lane, x, y);
         } else if (!slow && SPC5_BLR) {  // balanced lane ranges
             blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, a_bits,
                                                            a_rp, a_col, a_mask, a_val, lane, x, y);

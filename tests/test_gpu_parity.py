@@ -136,6 +136,22 @@ def test_spmv_repeatable_bitwise(spc5, name):
             assert spc5.spmv(s, x).tobytes() == y0.tobytes(), (name, r, vs)
 
 
+def test_lane_per_panel_split_chunks(spc5, monkeypatch):
+    """Lane-per-panel mode on split pieces of long panels (carry slots from that
+    mode), forced with the SPC5_LPR_SPLIT plan knob: same tolerance, repeatable."""
+    monkeypatch.setenv("SPC5_LPR_SPLIT", "1")
+    for name in ("longrows", "longrows_f32", "tall", "rand05"):
+        m = small_case(name)
+        x = case_x(name, m)
+        for r, vs, _ in fmt_keys(expected_small()["cases"][name]):
+            s = spc5.csr_to_spc5(m, r, vs)
+            y = spc5.spmv(s, x)
+            y_ref = np.zeros(m.num_rows, m.values.dtype)
+            oracle.spmv_spc5_scalar(oracle.csr_to_spc5(m, r, vs), x, y_ref)
+            assert_close(m, y, y_ref, x, f"{name} {r},{vs} lpr-split")
+            assert spc5.spmv(s, x).tobytes() == y.tobytes()
+
+
 def test_identity_exact_and_cancellation(spc5):
     m = small_case("identity32")
     x = np.random.default_rng(3).uniform(-1, 1, 32)
@@ -476,6 +492,53 @@ def _full_config_parity(spc5, cfg_id):
         scaled = oracle.scaled_error(m, y, x)
         assert float(scaled.max()) <= oracle.VERIFY_FACTOR, (r, vs)
         del s
+        torch.cuda.empty_cache()
+
+
+@pytest.mark.slow
+def test_config5_row_slices(spc5):
+    """BASELINE config 5 (stencil 400^3, 64M rows, 1.73G nnz) at full size on one
+    GPU, f64 and f32: device generator -> K1 -> K2; rows of three slices (start,
+    middle, end) checked against the oracle on host-generated rows, and y's
+    checksum against the exact GPU verifier over all rows."""
+    import torch
+    from paper_2307_14774_b200 import _native as nat
+    from paper_2307_14774_b200.workloads import stencil27_nnz, stencil27_rows, x_vector
+    from paper_2307_14774_b200.blocks import csr_to_spc5_device
+    n = 400
+    N = n ** 3
+    for prec, r, vs in (("f64", 1, 8), ("f32", 2, 16)):
+        tdt = torch.float64 if prec == "f64" else torch.float32
+        rp = torch.empty(N + 1, dtype=torch.int64, device="cuda")
+        nat.check(nat.lib.spc5_gen_stencil27_rowptr(n, 0, N, rp.data_ptr(), 0))
+        nnz = int(rp[-1])
+        assert nnz == stencil27_nnz(n)
+        ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        va = torch.empty(nnz, dtype=tdt, device="cuda")
+        nat.check(nat.lib.spc5_gen_stencil27_fill(n, 0, N, 1 if prec == "f64" else 0, 0, 27.0,
+                                                  rp.data_ptr(), ci.data_ptr(), va.data_ptr(), 0))
+        torch.cuda.synchronize()
+        s = csr_to_spc5_device(N, N, rp, ci, va, r, vs)
+        x = torch.from_numpy(x_vector(N, prec)).to("cuda")
+        y = torch.empty(N, dtype=tdt, device="cuda")
+        nat.check(nat.lib.spc5_spmv(s.handle().ptr, x.data_ptr(), y.data_ptr(), 0, 0))
+        ye = torch.empty(N, dtype=torch.float64, device="cuda")
+        ya = torch.empty(N, dtype=torch.float64, device="cuda")
+        nat.check(nat.lib.spc5_csr_exact(N, 1 if prec == "f64" else 0, rp.data_ptr(),
+                                         ci.data_ptr(), va.data_ptr(), x.data_ptr(),
+                                         ye.data_ptr(), ya.data_ptr(), 0))
+        err = ((y.to(torch.float64) - ye).abs() / ya.clamp(min=1e-300)).max().item()
+        assert err <= TOL[prec], (prec, err)
+        del ci, va, rp
+        xh, yh = x.cpu().numpy(), y.cpu().numpy()
+        for lo in (0, N // 2 - 1000, N - 3000):
+            m = stencil27_rows(n, lo, lo + 3000, prec)
+            ys = np.zeros(m.num_rows, dtype=xh.dtype)
+            oracle.spmv_spc5_scalar(oracle.csr_to_spc5(m, r, vs), xh, ys)
+            _, a = oracle.csr_reference(m, xh)
+            e = oracle.relative_error(yh[lo:lo + 3000], ys, a)
+            assert float(e.max()) <= TOL[prec], (prec, lo, float(e.max()))
+        del s, x, y, ye, ya
         torch.cuda.empty_cache()
 
 
