@@ -408,9 +408,20 @@ __device__ __forceinline__ uint32_t row_rt(const LaneMasks<LB> &mk, int rr) {
 template <typename T, typename MT, int R, int U>
 __device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s, int rr,
                                           uint32_t vaddr, uint32_t a_col, uint32_t a_mask,
-                                          const T *__restrict__ x) {
+                                          uint32_t a_zero, const T *__restrict__ x) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;
+    constexpr int N = LaneMasks<LB>::N;
+    constexpr uint32_t M = MB == 1 ? 0xffu : 0xffffu;
+    // this lane's row inside a block's packed masks, fixed for the chunk
+    const int bit = rr * 8 * MB;
+    uint32_t keep[N];  // bits of the rows below rr
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+        const int lo = i * 32;
+        keep[i] = bit >= lo + 32 ? 0xffffffffu : (bit <= lo ? 0u : ((1u << (bit - lo)) - 1u));
+    }
+    const int wsel = bit >> 5, sh = bit & 31;
     for (int j = 0; j < maxlen; j += U) {
         uint32_t col[U], vr[U], m[U];
         int h[U], cm = 0;
@@ -421,13 +432,21 @@ __device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s
             const uint32_t bk = (uint32_t)(ok ? s + j + k : 0);
             col[k] = lds_u32(a_col + bk * 4u);
             LaneMasks<LB> mk;
-            mk.load(a_mask + bk * LB);
-            mk.clear_if(ok);
+            mk.load(ok ? a_mask + bk * LB : a_zero);  // past the range: 16 zero bytes
             // block k's values: rows 0..R-1 in order; this lane's row starts
             // after the rows below it
-            vr[k] = vnext + (uint32_t)popc_below<LB, MB>(mk, rr) * (uint32_t)sizeof(T);
-            vnext += (uint32_t)mk.popc() * (uint32_t)sizeof(T);
-            m[k] = R == 1 ? mk.w[0] : row_rt<LB, MB>(mk, rr);
+            int below = 0, total = 0;
+#pragma unroll
+            for (int i = 0; i < N; ++i) {
+                total += __popc(mk.w[i]);
+                if (R > 1) below += __popc(mk.w[i] & keep[i]);
+            }
+            vr[k] = vnext + (uint32_t)below * (uint32_t)sizeof(T);
+            vnext += (uint32_t)total * (uint32_t)sizeof(T);
+            uint32_t w = mk.w[0];
+#pragma unroll
+            for (int i = 1; i < N; ++i) w = wsel == i ? mk.w[i] : w;
+            m[k] = R == 1 ? mk.w[0] : (w >> sh) & M;
             h[k] = __popc(m[k]);
             cm = max(cm, h[k]);
         }
@@ -438,7 +457,8 @@ __device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s
 
 template <typename T, typename MT, int R, bool GENERIC>
 __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int npc,
-                                          int lg, bool head_mid, uint32_t a_rec, uint32_t a_col, uint32_t a_mask,
+                                          int lg, bool head_mid, uint32_t a_zero, uint32_t a_rec,
+                                          uint32_t a_col, uint32_t a_mask,
                                           uint32_t a_val, int lane, const T *__restrict__ x,
                                           T *__restrict__ y) {
     constexpr int MB = (int)sizeof(MT);
@@ -483,11 +503,11 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t 
         // gathers are in flight before the first FMA; values still accumulate
         // in storage order
         if (maxlen <= 3) {
-            lpp_steps<T, MT, R, 3>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, x);
+            lpp_steps<T, MT, R, 3>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
         } else if (maxlen <= 6) {
-            lpp_steps<T, MT, R, 6>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, x);
+            lpp_steps<T, MT, R, 6>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
         } else {
-            lpp_steps<T, MT, R, 9>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, x);
+            lpp_steps<T, MT, R, 9>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
         }
         for (int o = 1; o < G; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
         const int64_t p = p0 + q;
@@ -880,7 +900,7 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
 
         if (flags & 4) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
-                                         a_rp, a_col, a_mask, a_val, lane, x, y);
+                                         sbase + 48, a_rp, a_col, a_mask, a_val, lane, x, y);
         } else if (!slow && SPC5_BLR) {  // balanced lane ranges
             blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, a_bits,
                                                            a_rp, a_col, a_mask, a_val, lane, x, y);
