@@ -699,7 +699,7 @@ __device__ __forceinline__ void blr_put(const SpmvArgs &a, int64_t c, int64_t p0
 #endif
 template <typename T, typename MT, int R, bool GENERIC, int U>
 __device__ __forceinline__ void blr_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int n,
-                                          bool head_mid, int sh0, uint32_t a_bits,
+                                          bool head_mid, int sh0, uint32_t a_zero, uint32_t a_bits,
                                           uint32_t a_lane, uint32_t a_col, uint32_t a_mask,
                                           uint32_t a_val, int lane, const T *__restrict__ x,
                                           T *__restrict__ y) {
@@ -728,14 +728,18 @@ __device__ __forceinline__ void blr_chunk(const SpmvArgs &a, int64_t c, int64_t 
         LaneMasks<LB> mk[U];
         bool st[U];
         uint32_t vnext = vaddr;
+        // panel-start bits of blocks sl+j .. sl+j+U-1 (two words, one funnel shift)
+        const int gb = sh0 + sl + j;
+        const uint32_t w0 = lds_u32(a_bits + (uint32_t)(gb >> 5) * 4u);
+        const uint32_t w1 = lds_u32(a_bits + (uint32_t)((gb >> 5) + 1) * 4u);
+        const uint32_t sbits = __funnelshift_r(w0, w1, gb & 31);
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             const bool ok = j + k < my;
             const int b = ok ? sl + j + k : 0;
             col[k] = lds_u32(a_col + (uint32_t)b * 4u);
-            mk[k].load(a_mask + (uint32_t)b * LB);
-            mk[k].clear_if(ok);
-            st[k] = ok && j + k > 0 && start_bit(b);
+            mk[k].load(ok ? a_mask + (uint32_t)b * LB : a_zero);
+            st[k] = ok && j + k > 0 && ((sbits >> k) & 1u);
             vbk[k] = vnext;
             vnext += (uint32_t)mk[k].popc() * (uint32_t)sizeof(T);
         }
@@ -902,7 +906,7 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
             lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
                                          sbase + 48, a_rp, a_col, a_mask, a_val, lane, x, y);
         } else if (!slow && SPC5_BLR) {  // balanced lane ranges
-            blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, a_bits,
+            blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, sbase + 48, a_bits,
                                                            a_rp, a_col, a_mask, a_val, lane, x, y);
         } else {
             constexpr int KW = R <= 2 ? 4 : (R == 4 ? 2 : 1);  // windows per step
