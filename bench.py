@@ -291,7 +291,7 @@ def reference_arm(args, formats):
     line = {"impl": "reference", "metric": "SpMV GFLOP/s (2*nnz/t)", "value": val,
             "unit": "GFLOP/s", "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": el / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak" if args.gpus == 1 else "strong", "vs_baseline": None,
+            "scaling": "strong", "vs_baseline": None,
             "dtype": CONFIGS[args.config]["precision"], "data": "synthetic",
             "config": {"workload": CONFIGS[args.config]["name"],
                        "formats": [fmt_key(*f) for f in formats]},
@@ -431,7 +431,7 @@ def ours_single(args, formats):
     line = {"metric": "SpMV GFLOP/s (2*nnz/t)", "value": value, "unit": "GFLOP/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
             "config": {"workload": cfgd["name"], "formats": [fmt_key(*f) for f in formats],
                        "num_rows": num_rows,
                        "nnz": mats[formats[0]].nnz,

@@ -123,18 +123,64 @@ def iterate_products(x0, steps: int, layout: ShardLayout, rank: int, world: int,
 
 
 # ----------------------------------------------------------------------------- bench
+def _shard_csr(cfg, lo, hi, prec):
+    """Device CSR of rows [lo, hi) of a BASELINE config (stencil / power-law / FEM)."""
+    import torch
+
+    from . import _native as nat
+    from .workloads import PL_N, PL_TABLE_BITS, powerlaw_len_table
+    tdt = torch.float64 if prec == "f64" else torch.float32
+    pc = 1 if prec == "f64" else 0
+    rows = hi - lo
+    rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
+    gen = cfg.get("gen", "stencil")
+    table = torch.from_numpy(powerlaw_len_table()).to("cuda") if gen == "powerlaw" else None
+    if gen == "stencil":
+        nat.check(nat.lib.spc5_gen_stencil27_rowptr(cfg["n"], lo, hi, rp.data_ptr(), 0))
+    elif gen == "powerlaw":
+        nat.check(nat.lib.spc5_gen_powerlaw_rowptr(PL_N, lo, hi, 0, table.data_ptr(),
+                                                   PL_TABLE_BITS, rp.data_ptr(), 0))
+    else:
+        nat.check(nat.lib.spc5_gen_fem_rowptr(cfg["rows"] // 3, lo, hi, rp.data_ptr(), 0))
+    nnz = int(rp[-1])
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
+    va = torch.empty(max(nnz, 1), dtype=tdt, device="cuda")
+    if gen == "stencil":
+        nat.check(nat.lib.spc5_gen_stencil27_fill(cfg["n"], lo, hi, pc, 0, 27.0, rp.data_ptr(),
+                                                  ci.data_ptr(), va.data_ptr(), 0))
+    elif gen == "powerlaw":
+        nat.check(nat.lib.spc5_gen_powerlaw_fill(PL_N, lo, hi, pc, 0, table.data_ptr(),
+                                                 PL_TABLE_BITS, rp.data_ptr(), ci.data_ptr(),
+                                                 va.data_ptr(), 0))
+    else:
+        nat.check(nat.lib.spc5_gen_fem_fill(cfg["rows"] // 3, lo, hi, pc, 0, rp.data_ptr(),
+                                            ci.data_ptr(), va.data_ptr(), 0))
+    torch.cuda.synchronize()
+    return rp, ci, va
+
+
 def bench_distributed(args, formats) -> None:
-    """bench.py for N > 1: config-2/5 stencil split over the ranks; one step is
-    one iterated product per format (local K2 + all-gather of x over NCCL)."""
+    """bench.py for N > 1 (one process per GPU, torchrun, NCCL).
+
+    The matrix's row panels are split nnz-balanced over the ranks
+    (panel_partition == partition_by_nnz); every rank converts only its rows.
+    One step = one product per format with x replicated and each rank writing
+    its own y-slice (no exchange needed: strong scaling of the same total
+    work as the 1-GPU line).  The iterated form (x <- A.x refreshed by the
+    NCCL all-gather of the y-slices, BASELINE config 5) is timed after it and
+    reported under "iterated".  Times are device times (CUDA events), the max
+    over ranks."""
     import json
     import os
     import time
 
+    import numpy as np
     import torch
     import torch.distributed as dist
 
     from . import _native as nat
     from .blocks import csr_to_spc5_device, filling_stats, torch_stream
+    from .kernels import spmv
     from .workloads import CONFIGS, x_vector
 
     rank = int(os.environ.get("RANK", "0"))
@@ -143,67 +189,141 @@ def bench_distributed(args, formats) -> None:
     torch.cuda.set_device(local)
     dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = CONFIGS[args.config]
-    if "n" not in cfg:
-        raise SystemExit("multi-GPU bench supports the stencil configs (2, 5)")
-    n = cfg["n"]
-    N = n ** 3
+    if cfg.get("gen") is None and "n" not in cfg:
+        raise SystemExit(f"config {args.config}: no device generator for the multi-GPU bench")
     prec = cfg["precision"]
     tdt = torch.float64 if prec == "f64" else torch.float32
     vb = 8 if prec == "f64" else 4
-    rp_all = torch.empty(N + 1, dtype=torch.int64, device="cuda")
-    nat.check(nat.lib.spc5_gen_stencil27_rowptr(n, 0, N, rp_all.data_ptr(), 0))
-    x0 = torch.from_numpy(x_vector(N, prec)).to("cuda")
-    results = {}
+    N = cfg["n"] ** 3 if "n" in cfg else cfg["rows"]
+    C = N if "n" in cfg else cfg["cols"]
+    # global row pointers (structure only) for the partition
+    rp_all, ci_all, va_all = _shard_csr(cfg, 0, N, prec)
+    del ci_all, va_all
+    torch.cuda.empty_cache()
+    x_np = x_vector(C, prec)
+    x0 = torch.from_numpy(x_np).to("cuda")
+    st = torch_stream()
+    stream = torch.cuda.current_stream()
+    results, launches = {}, 0
+    from bench import ClockSampler, peaks  # noqa: E402  (repo root on sys.path)
+    sampler = ClockSampler(local) if rank == 0 else None
     for (r, vs) in formats:
         layout = shard_layout(rp_all, r, world)
         lo, hi = layout.rows(rank)
-        rows = hi - lo
-        rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
-        nat.check(nat.lib.spc5_gen_stencil27_rowptr(n, lo, hi, rp.data_ptr(), 0))
-        nnz = int(rp[-1])
-        ci = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
-        va = torch.empty(max(nnz, 1), dtype=tdt, device="cuda")
-        nat.check(nat.lib.spc5_gen_stencil27_fill(n, lo, hi, 1 if prec == "f64" else 0, 0, 27.0,
-                                                  rp.data_ptr(), ci.data_ptr(), va.data_ptr(), 0))
-        torch.cuda.synchronize()
-        s = csr_to_spc5_device(rows, N, rp, ci, va, r, vs)
+        rp, ci, va = _shard_csr(cfg, lo, hi, prec)
+        s = csr_to_spc5_device(hi - lo, C, rp, ci, va, r, vs)
         del rp, ci, va
+        torch.cuda.empty_cache()
         h = s.handle()
-        nnz_all = torch.tensor([h.info.nnz], device="cuda")
-        dist.all_reduce(nnz_all)
+        y = torch.empty(max(hi - lo, 1), dtype=tdt, device="cuda")
+        counts = torch.tensor([h.info.nnz, filling_stats(s).footprint_bytes + vb * (hi - lo)],
+                              dtype=torch.int64, device="cuda")
+        dist.all_reduce(counts)
+        nnz_all, bytes_all = int(counts[0]), int(counts[1]) + vb * C * world
 
-        def local_spmv(xf, yout, h=h):
-            nat.check(nat.lib.spc5_spmv(h.ptr, xf.data_ptr(), yout.data_ptr(), 0, torch_stream()))
+        def product():
+            nat.check(nat.lib.spc5_spmv(h.ptr, x0.data_ptr(), y.data_ptr(), 0, st))
+            return nat.last_launch_count()
 
-        # rescale by an exact power of two each step so 100 iterations stay finite
-        scale = 1.0 / 64.0
         for _ in range(args.warmup):
-            iterate_products(x0, 1, layout, rank, world, local_spmv, scale)
+            product()
         torch.cuda.synchronize()
         dist.barrier()
+        if sampler is not None and not results:
+            sampler.start()
+            time.sleep(0.3)
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record()
-        iterate_products(x0, args.steps, layout, rank, world, local_spmv, scale)
-        e1.record()
+        e0.record(stream)
+        for _ in range(args.steps):
+            launches += product()
+        e1.record(stream)
         torch.cuda.synchronize()
         el = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
         dist.all_reduce(el, op=dist.ReduceOp.MAX)
         dist.barrier()
-        results[f"b({r},{vs})"] = {"seconds": float(el), "nnz": int(nnz_all),
-                                   "local_footprint": filling_stats(s).footprint_bytes}
-        del s, h
+
+        # iterated products: local K2 into the next x buffer + all-gather of the slices
+        def local_spmv(xf, yout, h=h):
+            nat.check(nat.lib.spc5_spmv(h.ptr, xf.data_ptr(), yout.data_ptr(), 0, st))
+
+        iters = max(3, min(args.steps, 20))
+        iterate_products(x0, 2, layout, rank, world, local_spmv, 1.0 / 64.0)
+        torch.cuda.synchronize()
+        dist.barrier()
+        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        i0.record(stream)
+        iterate_products(x0, iters, layout, rank, world, local_spmv, 1.0 / 64.0)
+        i1.record(stream)
+        torch.cuda.synchronize()
+        it = torch.tensor([i0.elapsed_time(i1) * 1e-3], device="cuda")
+        dist.all_reduce(it, op=dist.ReduceOp.MAX)
+
+        # end to end through the public API on pinned host buffers
+        xp = torch.empty(C, dtype=tdt, pin_memory=True)
+        xp.numpy()[:] = x_np
+        yp = torch.empty(max(hi - lo, 1), dtype=tdt, pin_memory=True)
+        e2e_steps = max(3, min(args.steps, 20))
+        spmv(s, xp.numpy(), yp.numpy()[:hi - lo])
+        dist.barrier()
+        t0 = time.perf_counter()
+        for _ in range(e2e_steps):
+            spmv(s, xp.numpy(), yp.numpy()[:hi - lo])
+        te = torch.tensor([time.perf_counter() - t0], device="cuda")
+        dist.all_reduce(te, op=dist.ReduceOp.MAX)
+        results[f"b({r},{vs})"] = {"seconds": float(el), "nnz": nnz_all, "bytes": bytes_all,
+                                   "iter_seconds": float(it), "iters": iters,
+                                   "e2e_seconds": float(te), "e2e_steps": e2e_steps,
+                                   "h2d": vb * C, "d2h": vb * (hi - lo)}
+        del s, h, y
         torch.cuda.empty_cache()
+    clocks = sampler.stop() if sampler is not None else None
+    h2d = torch.tensor([sum(v["h2d"] for v in results.values())], device="cuda")
+    d2h = torch.tensor([sum(v["d2h"] for v in results.values())], device="cuda")
+    dist.all_reduce(h2d)
+    dist.all_reduce(d2h)
+    lc = torch.tensor([launches], device="cuda")
+    dist.all_reduce(lc)
     if rank == 0:
-        tot_flops = sum(2.0 * v["nnz"] * args.steps for v in results.values())
+        peak, peak_kind = peaks()
+        flops = sum(2.0 * v["nnz"] for v in results.values())
         tot_t = sum(v["seconds"] for v in results.values())
-        line = {"metric": "SpMV GFLOP/s (2*nnz/t)", "value": tot_flops / tot_t / 1e9,
-                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-                "ms_per_step": tot_t / args.steps * 1e3, "higher_is_better": True,
-                "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+        tot_b = sum(v["bytes"] for v in results.values()) * args.steps
+        achieved = tot_b / tot_t / 1e9
+        line = {"metric": "SpMV GFLOP/s (2*nnz/t)", "value": flops * args.steps / tot_t / 1e9,
+                "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
+                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "dtype": prec, "data": "synthetic",
                 "config": {"workload": cfg["name"], "formats": list(results),
-                           "step": "x <- A.x per format: local K2 + allgather of x (NCCL)",
-                           "parallelism": f"row-panel shards x{world}"},
-                "formats": {k: {"gflops": 2.0 * v["nnz"] * args.steps / v["seconds"] / 1e9}
-                            for k, v in results.items()}}
+                           "num_rows": N, "nnz": results[next(iter(results))]["nnz"],
+                           "step": "y_f = A_f.x for every format; x replicated, each rank "
+                                   "writes its nnz-balanced row-panel slice of y",
+                           "order": "the K products of each format run back to back",
+                           "l2": "inputs larger than L2 (no flush)",
+                           "parallelism": f"row-panel shards x{world} (partition_by_nnz)"},
+                "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world,
+                             "unit": "GB/s", "frac": achieved / (peak * world),
+                             "traffic": None,
+                             "peak_source": f"{peak_kind} hbm_gbs x {world} GPUs",
+                             "alg_bytes_per_step": sum(v["bytes"] for v in results.values())},
+                "formats": {k: {"gflops": 2.0 * v["nnz"] * args.steps / v["seconds"] / 1e9,
+                                "us": v["seconds"] / args.steps * 1e6,
+                                "iterated_gflops": 2.0 * v["nnz"] * v["iters"]
+                                / v["iter_seconds"] / 1e9,
+                                "iterated_us": v["iter_seconds"] / v["iters"] * 1e6}
+                            for k, v in results.items()},
+                "iterated": {"step": "x <- A.x/64: local K2 into the next x + NCCL all-gather "
+                                     "of the y-slices (BASELINE config 5 form)",
+                             "value": flops * sum(v["iters"] for v in results.values())
+                             / len(results) / sum(v["iter_seconds"] for v in results.values())
+                             / 1e9, "unit": "GFLOP/s"},
+                "gpu_launches": int(lc),
+                "clocks": clocks,
+                "e2e": {"value": sum(2.0 * v["nnz"] * v["e2e_steps"] for v in results.values())
+                        / sum(v["e2e_seconds"] for v in results.values()) / 1e9,
+                        "unit": "GFLOP/s", "h2d_bytes_per_step": int(h2d),
+                        "d2h_bytes_per_step": int(d2h),
+                        "path": "paper_2307_14774_b200.spmv(numpy pinned) per rank, max over ranks"},
+                "cpu_baseline": None}
         print(json.dumps(line), flush=True)
     dist.destroy_process_group()
