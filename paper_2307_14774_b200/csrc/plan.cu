@@ -282,7 +282,7 @@ __device__ __forceinline__ void blob_shape(int64_t b0, int64_t b1, int64_t npc, 
                                            int off32, int64_t *nwords, int64_t *nrec) {
     const bool lpr = flags & 4;
     *nwords = (!lpr && b1 > b0) ? ((b1 - 1 + off32) >> 5) - ((b0 + off32) >> 5) + 1 : 0;
-    *nrec = lpr ? npc + 1 : 32;
+    *nrec = lpr ? npc * (1 << ((flags >> 3) & 3)) + 1 : 32;  // G sub-ranges per panel
 }
 __device__ __forceinline__ int64_t a16_dev(int64_t v) { return (v + 15) / 16 * 16; }
 
@@ -362,23 +362,34 @@ __global__ void blob_fill_kernel(int64_t nc, int r, int vs, int off32,
             rec[lane] = (uint32_t)(vin - cnt) | ((uint32_t)first << 16);
             continue;
         }
+        // entry t = q*G + sub: start of sub-range sub of panel p0+q (G contiguous
+        // block ranges, ceil(len/G) blocks each), last entry = chunk end
+        const int lg = (f >> 3) & 3, G = 1 << lg;
         uint32_t running = 0;
-        for (int64_t q0 = 0; q0 < nr; q0 += 32) {
-            const int64_t q = q0 + lane;
-            // panel p0+q's blocks inside the chunk: [max(rowptr, b0), min(rowptr', b1))
-            const int64_t s = q < nr ? min(max(rowptr[p0 + q], b0), b1) - b0 : 0;
+        for (int64_t t0 = 0; t0 < nr; t0 += 32) {
+            const int64_t t = t0 + lane;
+            auto start = [&](int64_t tt) -> int64_t {  // block offset of entry tt
+                if (tt >= nr - 1) return b1 - b0;
+                const int64_t q = tt >> lg, sub = tt & (G - 1);
+                // panel p0+q's blocks inside the chunk: [max(rowptr, b0), min(rowptr', b1))
+                const int64_t ps = min(max(rowptr[p0 + q], b0), b1) - b0;
+                const int64_t pe2 = min(rowptr[p0 + q + 1], b1) - b0;
+                const int64_t len = pe2 - ps, per = (len + G - 1) >> lg;
+                return ps + min(sub * per, len);
+            };
+            const int64_t s = t < nr ? start(t) : 0;
             int cnt = 0;
-            if (q < nr - 1) {
-                const int64_t e = min(rowptr[p0 + q + 1], b1);
-                for (int64_t b = b0 + s; b < e; ++b)
+            if (t < nr - 1) {
+                const int64_t e = start(t + 1);
+                for (int64_t b = b0 + s; b < b0 + e; ++b)
                     for (int rr = 0; rr < r; ++rr) cnt += __popc(load_mask(masks, b * r + rr, vs));
             }
             int incl = cnt;
             for (int d = 1; d < 32; d <<= 1) {
-                const int t = __shfl_up_sync(0xffffffffu, incl, d);
-                if (lane >= d) incl += t;
+                const int tv = __shfl_up_sync(0xffffffffu, incl, d);
+                if (lane >= d) incl += tv;
             }
-            if (q < nr) rec[q] = (uint32_t)s | ((running + (uint32_t)(incl - cnt)) << 16);
+            if (t < nr) rec[t] = (uint32_t)s | ((running + (uint32_t)(incl - cnt)) << 16);
             running += (uint32_t)__shfl_sync(0xffffffffu, incl, 31);
         }
     }
@@ -414,7 +425,8 @@ __global__ void lpp_panels_kernel(int64_t nc, const int64_t *__restrict__ chunk_
                                   const uint8_t *__restrict__ flags, unsigned long long *out) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c < nc && (flags[c] & 4))
-        atomicMax(out, (unsigned long long)(chunk_p[c + 1] - chunk_p[c] + ((flags[c] >> 5) & 1)));
+        atomicMax(out, (unsigned long long)((chunk_p[c + 1] - chunk_p[c] + ((flags[c] >> 5) & 1))
+                                            << ((flags[c] >> 3) & 3)));
 }
 
 __global__ void narrow_kernel(const int64_t *in, int64_t n, int *out) {

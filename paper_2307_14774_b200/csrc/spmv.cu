@@ -401,9 +401,9 @@ __device__ __forceinline__ uint32_t row_rt(const LaneMasks<LB> &mk, int rr) {
 // block ranges of the panel, in storage order, and the G partial sums of a
 // row meet in a butterfly (G = 1 << lg, chunk flag bits 3-4).  The 32/(R*G)
 // groups of a step touch consecutive panels (neighbouring x for banded
-// matrices).  The plan's panel records give each panel's first block and
-// first value inside the chunk (16 bits each), so a lane starts at once;
-// with G > 1 the lanes of a row also count their sub-ranges' values.
+// matrices).  The plan's records give the first block and first value
+// (16 bits each, relative to the chunk) of every (panel, sub-range), so a
+// lane starts at once.
 // Lane's row over blocks s .. s+my-1 of its panel range, U blocks per step.
 template <typename T, typename MT, int R, int U>
 __device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s, int rr,
@@ -472,30 +472,13 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t 
     for (int q0 = 0; q0 < npc; q0 += PP) {
         const int q = q0 + grp;
         const bool pv = q < npc;
-        const uint32_t rq = a_rec + (uint32_t)min(q, npc - 1) * 4u;
+        // this lane's block range and first value: entries t, t+1 of the
+        // plan's records (t = q*G + sub)
+        const uint32_t rq = a_rec + (uint32_t)((min(q, npc - 1) << lg) + sub) * 4u;
         const uint32_t r0 = lds_u32(rq), r1 = lds_u32(rq + 4u);
-        const int s0 = (int)(r0 & 0xffffu);
-        const int len = pv ? (int)(r1 & 0xffffu) - s0 : 0;
-        int s = s0, my = len;
-        uint32_t vofs = r0 >> 16;
-        if (G > 1) {  // sub-range of the panel and the values before it
-            const int per = (len + G - 1) >> lg;
-            const int lo = min(sub * per, len);
-            my = min(lo + per, len) - lo;
-            s = s0 + lo;
-            int cnt = 0;  // values of this lane's range (all R rows)
-            for (int j = 0; j < my; ++j) {
-                LaneMasks<LB> mk;
-                mk.load(a_mask + (uint32_t)(s + j) * LB);
-                cnt += mk.popc();
-            }
-            int incl = cnt;  // inclusive scan over the G lanes of the row
-            for (int d = 1; d < G; d <<= 1) {
-                const int t = __shfl_up_sync(kFull, incl, d);
-                if (sub >= d) incl += t;
-            }
-            vofs += (uint32_t)(incl - cnt);
-        }
+        const int s = (int)(r0 & 0xffffu);
+        const int my = pv ? (int)(r1 & 0xffffu) - s : 0;
+        const uint32_t vofs = r0 >> 16;
         const int maxlen = __reduce_max_sync(kFull, my);
         uint32_t vaddr = a_val + vofs * (uint32_t)sizeof(T);
         double acc = 0.0;
