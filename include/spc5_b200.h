@@ -118,6 +118,18 @@ int spc5_device_arrays(spc5_matrix_t m, const int64_t **rowptr, const uint32_t *
 int spc5_spmv(spc5_matrix_t m, const void *d_x, void *d_y, int accumulate, void *stream);
 
 /*
+ * Iterated products over several GPUs, fused exchange: y = scale * A.x on
+ * this rank's row shard (y = its slice of the next x), and every stored row
+ * is also written to d_peer_bases[k][row0 + row] -- the next-x buffers of
+ * the peer GPUs (NVLink peer or symmetric-memory pointers), so no separate
+ * all-gather follows the product.  scale should be exact (a power of two).
+ * The caller orders iterations with a cross-GPU barrier.  Replaces the
+ * product + allgather of the iterated config-5 form.
+ */
+int spc5_spmv_mirrored(spc5_matrix_t m, const void *d_x, void *d_y, double scale,
+                       const void *const *d_peer_bases, int npeers, int64_t row0, void *stream);
+
+/*
  * Same product restricted to the panel range [panel_lo, panel_hi): rows
  * [panel_lo*r, min(panel_hi*r, num_rows)) of y are written, nothing else.
  * One worker of spmv_parallel (parallel.py:55-92); results are bitwise equal

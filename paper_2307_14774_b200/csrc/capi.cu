@@ -268,6 +268,24 @@ int spc5_spmv(spc5_matrix_t h, const void *d_x, void *d_y, int accumulate, void 
     return launch_spmv(h->m, 0, h->m.num_panels, d_x, d_y, accumulate, st);
 }
 
+int spc5_spmv_mirrored(spc5_matrix_t h, const void *d_x, void *d_y, double scale,
+                       const void *const *d_peer_bases, int npeers, int64_t row0, void *stream) {
+    g_launches = 0;
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    if ((!d_x && h->m.num_cols) || (!d_y && h->m.num_rows))
+        return fail(SPC5_EINVAL, "x/y must be non-null");
+    if (npeers < 0 || npeers > 8 || (npeers && !d_peer_bases))
+        return fail(SPC5_EINVAL, "npeers must be in [0, 8] with a peer pointer array");
+    Mirror mi;
+    mi.n = npeers;
+    for (int k = 0; k < npeers; ++k) mi.ptr[k] = const_cast<void *>(d_peer_bases[k]);
+    mi.row0 = row0;
+    mi.scale = scale;
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SPC5_TRY(ensure_plan(h, st));
+    return launch_spmv(h->m, 0, h->m.num_panels, d_x, d_y, 0, st, &mi);
+}
+
 int spc5_spmv_panels(spc5_matrix_t h, int64_t panel_lo, int64_t panel_hi, const void *d_x,
                      void *d_y, int accumulate, void *stream) {
     g_launches = 0;

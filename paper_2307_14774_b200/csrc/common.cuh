@@ -96,8 +96,15 @@ int convert_csr(Matrix &m, const int64_t *d_row_ptr, const int32_t *d_col_idx,
                 const void *d_values, cudaStream_t st);
 int build_plan(Matrix &m, bool validate, cudaStream_t st);
 void free_plan(Plan &p);
+// fused exchange of iterated products: y rows also stored at ptr[i][row0 + row]
+struct Mirror {
+    void *ptr[8];
+    int n = 0;
+    int64_t row0 = 0;
+    double scale = 1.0;
+};
 int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void *y,
-                int accumulate, cudaStream_t st);
+                int accumulate, cudaStream_t st, const Mirror *mirror = nullptr);
 int partition_by_nnz(const Matrix &m, int workers, int64_t *h_ranges, cudaStream_t st);
 int block_value_offsets(const Matrix &m, int64_t *d_offsets, cudaStream_t st);
 int validate_structure(const Matrix &m, cudaStream_t st);

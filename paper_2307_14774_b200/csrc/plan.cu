@@ -258,7 +258,7 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
         const int64_t npc = hi_p - lo_p + (ends_clean ? 0 : 1);
         // split pieces of long panels run faster in balanced-lane-range mode
         const bool whole = !(f & 1) && ends_clean;
-        if ((whole || lpr_split) && npc > 0 && npc * r <= 32 * 64) {
+        if ((whole || lpr_split) && lpr_split >= 0 && npc > 0 && npc * r <= 32 * 64) {
             int64_t maxlen = 0;
             for (int64_t p = lo_p; p < lo_p + npc; ++p)
                 maxlen = max(maxlen, min(rowptr[p + 1], cb1) - max(rowptr[p], cb0));
@@ -735,7 +735,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
-            P.num_empty, getenv("SPC5_LPR_SPLIT") ? 1 : 0, P.chunk_flags);
+            P.num_empty, getenv("SPC5_NO_LPR") ? -1 : (getenv("SPC5_LPR_SPLIT") ? 1 : 0),
+            P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
         unsigned long long *d_st = nullptr, h_st[3] = {0, 0, 0};
         SPC5_TRY(dev_alloc(&d_st, 3));

@@ -35,6 +35,8 @@
 namespace spc5 {
 namespace {
 
+constexpr int kMaxMirrors = 8;  // peer buffers of the fused exchange
+
 struct SpmvArgs {
     const int64_t *rowptr;
     const uint32_t *colidx;
@@ -58,6 +60,13 @@ struct SpmvArgs {
     const uint8_t *blob;      // per-chunk metadata blobs (header, panel-start words, records)
     const uint4 *issue_rec;   // per chunk: bulk-copy sources / sizes (plan.cu issue_rec_kernel)
     int nslot;                // ring slots per warp (2..kMaxSlots)
+    // fused exchange (iterated products over GPUs): every y row is also
+    // stored, scaled, at mirror[i][mirror_row0 + row] (peer GPUs' next-x
+    // buffers over NVLink); y itself is scaled by yscale (1 unless mirrored)
+    void *mirror[kMaxMirrors];
+    int nmirror;
+    int64_t mirror_row0;
+    double yscale;
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -213,16 +222,21 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
     return v;
 }
 
+// one y row: y[row] (+)= v, mirrored to the peer buffers of the fused exchange
+template <typename T>
+__device__ __forceinline__ void put_row(const SpmvArgs &a, T *y, int64_t row, double v) {
+    T sv = (T)(v * a.yscale);
+    if (a.accumulate) sv = y[row] + sv;
+    y[row] = sv;
+    for (int i = 0; i < a.nmirror; ++i) static_cast<T *>(a.mirror[i])[a.mirror_row0 + row] = sv;
+}
 template <typename T, int G>
-__device__ __forceinline__ void store_rows(T *y, int64_t row0, int64_t num_rows, const double *acc,
-                                           int accumulate) {
+__device__ __forceinline__ void store_rows(const SpmvArgs &a, T *y, int64_t row0,
+                                           const double *acc) {
 #pragma unroll
     for (int g = 0; g < G; ++g) {
         const int64_t row = row0 + g;
-        if (row < num_rows) {
-            const T sv = (T)acc[g];
-            y[row] = accumulate ? y[row] + sv : sv;
-        }
+        if (row < a.num_rows) put_row<T>(a, y, row, acc[g]);
     }
 }
 
@@ -499,8 +513,7 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t 
             if (q == 0 && head_mid) {  // head of a split panel: carry slot, fixup adds it
                 a.carry[c * R + rr] = acc;
             } else if (row < a.num_rows && (!GENERIC || (p >= a.p_lo && p < a.p_hi))) {
-                const T sv = (T)acc;
-                y[row] = a.accumulate ? y[row] + sv : sv;
+                put_row<T>(a, y, row, acc);
             }
         }
     }
@@ -614,8 +627,7 @@ __device__ __forceinline__ void lpb_chunk(const SpmvArgs &a, int64_t c, int64_t 
 #pragma unroll
                         for (int g = 0; g < R; ++g) a.carry[c * R + g] = carry[g];
                     } else {
-                        store_rows<T, R>(y, (p0 + carry_panel) * R, a.num_rows, carry,
-                                         a.accumulate);
+                        store_rows<T, R>(a, y, (p0 + carry_panel) * R, carry);
                     }
                 }
                 carry_valid = false;
@@ -638,7 +650,7 @@ __device__ __forceinline__ void lpb_chunk(const SpmvArgs &a, int64_t c, int64_t 
 #pragma unroll
                     for (int g = 0; g < R; ++g) a.carry[c * R + g] = s[g];
                 } else {
-                    store_rows<T, R>(y, (p0 + pl[k]) * R, a.num_rows, s, a.accumulate);
+                    store_rows<T, R>(a, y, (p0 + pl[k]) * R, s);
                 }
             }
             if (last) break;
@@ -671,7 +683,7 @@ __device__ __forceinline__ void blr_put(const SpmvArgs &a, int64_t c, int64_t p0
     }
     const int64_t P = p0 + p;
     if (generic && (P < a.p_lo || P >= a.p_hi)) return;
-    store_rows<T, R>(y, P * R, a.num_rows, v, a.accumulate);
+    store_rows<T, R>(a, y, P * R, v);
 }
 
 #ifndef SPC5_BLR
@@ -834,7 +846,7 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
             if (GENERIC && (p < a.p_lo || p >= a.p_hi)) continue;
 #pragma unroll
             for (int rr = 0; rr < R; ++rr)
-                if (p * R + rr < a.num_rows) y[p * R + rr] = T(0);
+                if (p * R + rr < a.num_rows) put_row<T>(a, y, p * R + rr, 0.0);
         }
     }
 
@@ -911,29 +923,35 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
 
 template <typename T, int R>
 __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_split,
-                             const int64_t *__restrict__ chunk_p, const double *__restrict__ carry,
-                             T *y, int64_t num_rows, int64_t c_lo, int64_t c_hi, int64_t p_lo,
-                             int64_t p_hi) {
+                             const int64_t *__restrict__ chunk_p, const SpmvArgs a) {
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= num_split) return;
     const int64_t c = split[i];
-    if (c < c_lo || c >= c_hi) return;
+    if (c < a.c_lo || c >= a.c_hi) return;
     const int64_t P = chunk_p[c];
-    if (P < p_lo || P >= p_hi) return;
+    if (P < a.p_lo || P >= a.p_hi) return;
     if (i > 0 && split[i - 1] == c - 1 && chunk_p[c - 1] == P) return;  // not the first
     double s[R];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) s[rr] = carry[c * R + rr];
+    for (int rr = 0; rr < R; ++rr) s[rr] = a.carry[c * R + rr];
     for (int64_t j = i + 1; j < num_split; ++j) {
         const int64_t cj = split[j];
-        if (cj != split[j - 1] + 1 || cj >= c_hi || chunk_p[cj] != P) break;
+        if (cj != split[j - 1] + 1 || cj >= a.c_hi || chunk_p[cj] != P) break;
 #pragma unroll
-        for (int rr = 0; rr < R; ++rr) s[rr] += carry[cj * R + rr];
+        for (int rr = 0; rr < R; ++rr) s[rr] += a.carry[cj * R + rr];
     }
+    // y already holds the panel's first-chunk part: add the carries (scaled
+    // like every stored row) and mirror the result
+    T *y = static_cast<T *>(a.y);
 #pragma unroll
     for (int rr = 0; rr < R; ++rr) {
         const int64_t row = P * R + rr;
-        if (row < num_rows) y[row] = y[row] + (T)s[rr];
+        if (row < a.num_rows) {
+            const T sv = y[row] + (T)(s[rr] * a.yscale);
+            y[row] = sv;
+            for (int k = 0; k < a.nmirror; ++k)
+                static_cast<T *>(a.mirror[k])[a.mirror_row0 + row] = sv;
+        }
     }
 }
 
@@ -971,8 +989,7 @@ int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
         SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, a, a.c_hi - a.c_lo, st));
     if (P.num_split) {
         fixup_kernel<T, R><<<(unsigned)cdiv(P.num_split, 128), 128, 0, st>>>(
-            P.split_chunks, P.num_split, P.chunk_p, P.carry, static_cast<T *>(a.y), m.num_rows,
-            a.c_lo, a.c_hi, a.p_lo, a.p_hi);
+            P.split_chunks, P.num_split, P.chunk_p, a);
         SPC5_CUDA(cudaGetLastError());
         ++launches;
     }
@@ -993,9 +1010,18 @@ int dispatch_r(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
 }  // namespace
 
 int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void *y,
-                int accumulate, cudaStream_t st) {
+                int accumulate, cudaStream_t st, const Mirror *mirror) {
     const Plan &P = m.plan;
     SpmvArgs a{};
+    a.yscale = 1.0;
+    if (mirror) {
+        if (mirror->n < 0 || mirror->n > kMaxMirrors)
+            return fail(SPC5_EINVAL, "at most 8 mirror buffers");
+        a.nmirror = mirror->n;
+        for (int i = 0; i < mirror->n; ++i) a.mirror[i] = mirror->ptr[i];
+        a.mirror_row0 = mirror->row0;
+        a.yscale = mirror->scale;
+    }
     a.rowptr = m.rowptr;
     a.colidx = m.colidx;
     a.masks = m.masks;

@@ -28,7 +28,7 @@ from typing import Callable
 import numpy as np
 
 __all__ = ["panel_partition", "ShardLayout", "shard_layout", "allgather_slices",
-           "iterate_products", "bench_distributed"]
+           "iterate_products", "FusedExchange", "iterate_products_fused", "bench_distributed"]
 
 
 def panel_partition(row_ptr, r: int, workers: int) -> list[tuple[int, int]]:
@@ -120,6 +120,56 @@ def iterate_products(x0, steps: int, layout: ShardLayout, rank: int, world: int,
         allgather_slices(xb, layout, rank, world)
         xa, xb = xb, xa
     return xa
+
+
+class FusedExchange:
+    """Symmetric-memory x buffers for iterated products with the exchange fused
+    into K2 (spc5_spmv_mirrored).  Set up once (allocation + rendezvous), then
+    run() any number of iterations: K2 stores every row of this rank's slice
+    into its own next-x buffer and, over NVLink, into every peer's (no
+    all-gather after the product); a device-side barrier on the symmetric
+    handle orders iterations."""
+
+    def __init__(self, n: int, dtype, layout: ShardLayout, rank: int, group=None):
+        import ctypes
+
+        import torch
+        import torch.distributed as dist
+        import torch.distributed._symmetric_memory as symm
+        group = group or dist.group.WORLD
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.bufs = [symm.empty(n, dtype=dtype, device=dev) for _ in range(2)]
+        self.hdls = [symm.rendezvous(b, group) for b in self.bufs]
+        self.lo, _ = layout.rows(rank)
+        self.esz = self.bufs[0].element_size()
+        self.peers = []
+        for h in self.hdls:
+            ptrs = [int(p) for i, p in enumerate(h.buffer_ptrs) if i != rank]
+            self.peers.append(((ctypes.c_void_p * max(len(ptrs), 1))(*ptrs), len(ptrs)))
+
+    def run(self, handle, x0, steps: int, scale: float = 1.0):
+        from . import _native as nat
+        from .blocks import torch_stream
+        self.bufs[0].copy_(x0)
+        self.hdls[0].barrier(channel=0)
+        cur = 0
+        for _ in range(steps):
+            nxt = 1 - cur
+            arr, npeer = self.peers[nxt]
+            nat.check(nat.lib.spc5_spmv_mirrored(
+                handle.ptr, self.bufs[cur].data_ptr(),
+                self.bufs[nxt].data_ptr() + self.lo * self.esz, float(scale), arr, npeer,
+                self.lo, torch_stream()))
+            self.hdls[nxt].barrier(channel=0)
+            cur = nxt
+        return self.bufs[cur]
+
+
+def iterate_products_fused(x0, steps: int, layout: ShardLayout, rank: int, world: int, handle,
+                           scale: float = 1.0, group=None):
+    """x_{t+1} = scale * A x_t with the exchange fused into K2 (see FusedExchange)."""
+    ex = FusedExchange(x0.numel(), x0.dtype, layout, rank, group)
+    return ex.run(handle, x0, steps, scale).clone()
 
 
 # ----------------------------------------------------------------------------- bench
@@ -257,6 +307,25 @@ def bench_distributed(args, formats) -> None:
         torch.cuda.synchronize()
         it = torch.tensor([i0.elapsed_time(i1) * 1e-3], device="cuda")
         dist.all_reduce(it, op=dist.ReduceOp.MAX)
+        # the same iterations with the exchange fused into K2 (NVLink stores)
+        fused = None
+        try:
+            ex = FusedExchange(C, tdt, layout, rank)
+            xf = ex.run(h, x0, iters, 1.0 / 64.0).clone()
+            xr = iterate_products(x0, iters, layout, rank, world, local_spmv, 1.0 / 64.0)
+            agree = bool(torch.equal(xf, xr))
+            torch.cuda.synchronize()
+            dist.barrier()
+            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            f0.record(stream)
+            ex.run(h, x0, iters, 1.0 / 64.0)
+            f1.record(stream)
+            torch.cuda.synchronize()
+            ft = torch.tensor([f0.elapsed_time(f1) * 1e-3], device="cuda")
+            dist.all_reduce(ft, op=dist.ReduceOp.MAX)
+            fused = {"seconds": float(ft), "bitwise_equal_to_allgather": agree}
+        except Exception as e:  # symmetric memory unavailable: report, keep the line
+            fused = {"error": f"{type(e).__name__}: {e}"[:200]}
 
         # end to end through the public API on pinned host buffers
         xp = torch.empty(C, dtype=tdt, pin_memory=True)
@@ -273,6 +342,7 @@ def bench_distributed(args, formats) -> None:
         results[f"b({r},{vs})"] = {"seconds": float(el), "nnz": nnz_all, "bytes": bytes_all,
                                    "iter_seconds": float(it), "iters": iters,
                                    "e2e_seconds": float(te), "e2e_steps": e2e_steps,
+                                   "fused": fused,
                                    "h2d": vb * C, "d2h": vb * (hi - lo)}
         del s, h, y
         torch.cuda.empty_cache()
@@ -310,7 +380,10 @@ def bench_distributed(args, formats) -> None:
                                 "us": v["seconds"] / args.steps * 1e6,
                                 "iterated_gflops": 2.0 * v["nnz"] * v["iters"]
                                 / v["iter_seconds"] / 1e9,
-                                "iterated_us": v["iter_seconds"] / v["iters"] * 1e6}
+                                "iterated_us": v["iter_seconds"] / v["iters"] * 1e6,
+                                "iterated_fused_us": (v["fused"]["seconds"] / v["iters"] * 1e6
+                                                      if "seconds" in v["fused"] else None),
+                                "fused": v["fused"]}
                             for k, v in results.items()},
                 "iterated": {"step": "x <- A.x/64: local K2 into the next x + NCCL all-gather "
                                      "of the y-slices (BASELINE config 5 form)",

@@ -552,3 +552,66 @@ def test_config3_full_size(spc5):
 def test_config4_full_size(spc5):
     """BASELINE config 4: FEM-like 786,432^2 with dense 3x3 blocks, f64, beta(4|8, 8)."""
     _full_config_parity(spc5, 4)
+
+
+# ---------------------------------------------------------------- fused exchange (iterated products)
+def test_spmv_mirrored_peer_stores(spc5):
+    """spc5_spmv_mirrored: y = scale*A.x and every row mirrored into each peer
+    buffer at row0 + row (here two plain device buffers stand in for peers)."""
+    import ctypes
+    import torch
+    from paper_2307_14774_b200 import _native as nat
+    from paper_2307_14774_b200.blocks import torch_stream
+    for name in ("longrows", "tall", "rand05"):
+        m = small_case(name)
+        x = torch.from_numpy(case_x(name, m)).cuda()
+        for r, vs in ((1, 8), (2, 4), (4, 16), (8, 8)):
+            s = spc5.csr_to_spc5(m, r, vs)
+            y = spc5.spmv(s, x)
+            row0 = 37
+            peers = [torch.full((m.num_rows + 100,), -7.0, dtype=x.dtype, device="cuda")
+                     for _ in range(2)]
+            arr = (ctypes.c_void_p * 2)(*[p.data_ptr() for p in peers])
+            ym = torch.empty_like(y)
+            nat.check(nat.lib.spc5_spmv_mirrored(s.handle().ptr, x.data_ptr(), ym.data_ptr(),
+                                                 0.25, arr, 2, row0, torch_stream()))
+            torch.cuda.synchronize()
+            assert torch.equal(ym, y * 0.25), (name, r, vs)
+            for p in peers:
+                assert torch.equal(p[row0:row0 + m.num_rows], ym), (name, r, vs)
+                assert bool((p[:row0] == -7.0).all()) and bool((p[row0 + m.num_rows:] == -7.0).all())
+
+
+def test_fused_iteration_single_rank(spc5):
+    """iterate_products_fused on a one-rank NCCL group (symmetric memory): the
+    same x as the all-gather form, bit for bit."""
+    import os
+    import torch
+    import torch.distributed as dist
+    from paper_2307_14774_b200.distributed import (iterate_products, iterate_products_fused,
+                                                   shard_layout)
+    from paper_2307_14774_b200 import _native as nat
+    from paper_2307_14774_b200.blocks import torch_stream
+    os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+    os.environ.setdefault("MASTER_PORT", "29533")
+    dist.init_process_group("nccl", rank=0, world_size=1,
+                            device_id=torch.device("cuda", torch.cuda.current_device()))
+    try:
+        from paper_2307_14774_b200.workloads import stencil27
+        m_sq = stencil27(12)  # square: x <- A.x iterates
+        x0 = torch.from_numpy(np.random.default_rng(3).uniform(-1, 1, m_sq.num_cols)).cuda()
+        for r, vs in ((1, 8), (4, 8)):
+            s = spc5.csr_to_spc5(m_sq, r, vs)
+            h = s.handle()
+            layout = shard_layout(m_sq.row_ptr, r, 1)
+
+            def local(xf, yout, h=h):
+                nat.check(nat.lib.spc5_spmv(h.ptr, xf.data_ptr(), yout.data_ptr(), 0,
+                                            torch_stream()))
+
+            xa = iterate_products(x0, 5, layout, 0, 1, local, 1.0 / 64.0)
+            xb = iterate_products_fused(x0, 5, layout, 0, 1, h, 1.0 / 64.0)
+            torch.cuda.synchronize()
+            assert torch.equal(xa, xb), (r, vs)
+    finally:
+        dist.destroy_process_group()
