@@ -236,7 +236,7 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                                    const int64_t *__restrict__ chunk_p,
                                    const int64_t *__restrict__ rowptr,
                                    const int64_t *__restrict__ empty, int64_t ne, int lpr_split,
-                                   uint8_t *flags) {
+                                   int lpr_bal_num, int lpr_bal_den, uint8_t *flags) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     uint8_t f = rowptr[chunk_p[c]] < chunk_b[c] ? 1 : 0;
@@ -265,7 +265,7 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
             int lg = 0;  // G = 1 << lg lanes per panel row, each with >= 1 block
             while (lg < 3 && npc * r * (2 << lg) <= 32 && maxlen >= (2 << lg)) ++lg;
             if (npc * r * (1 << lg) >= kLppMinLanes && maxlen <= 64 * (1 << lg) &&
-                maxlen * npc <= 2 * (cb1 - cb0) + 4 * npc)
+                maxlen * npc * lpr_bal_den <= lpr_bal_num * (cb1 - cb0) + 2 * lpr_bal_den * npc)
                 f |= 4 | (lg << 3) | (ends_clean ? 0 : 32);
         }
     }
@@ -730,13 +730,17 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     }
     int64_t slot_cap = 10 * 1024;  // target ring-slot size (tuning knob SPC5_SLOT_KB)
     if (const char *e = getenv("SPC5_SLOT_KB")) slot_cap = std::max(1, atoi(e)) * 1024;
+    // lane-per-panel chunks: the longest panel times the panel count may exceed
+    // the chunk's blocks by lpr_bal/4 (knob SPC5_LPR_BAL, quarters)
+    int lpr_bal = 4;
+    if (const char *e = getenv("SPC5_LPR_BAL")) lpr_bal = std::max(4, atoi(e));
     for (int64_t cb = 512;; cb >>= 1) {
         SPC5_TRY(build_chunks(m, cb, st));
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
             P.num_empty, getenv("SPC5_NO_LPR") ? -1 : (getenv("SPC5_LPR_SPLIT") ? 1 : 0),
-            P.chunk_flags);
+            lpr_bal, 4, P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
         unsigned long long *d_st = nullptr, h_st[3] = {0, 0, 0};
         SPC5_TRY(dev_alloc(&d_st, 3));

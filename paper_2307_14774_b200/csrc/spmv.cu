@@ -958,11 +958,18 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
 template <typename K>
 int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
                        cudaStream_t st) {
-    // 8 warps per CTA for small slots; 4 for large ones so several CTAs share an SM
-    int wpc = a.lay_bytes <= 6 * 1024 ? 8 : 4;
-    if (const char *e = getenv("SPC5_WPC")) wpc = std::min(8, std::max(1, atoi(e)));  // tuning knob
-    int S = 2;
-    if (const char *e = getenv("SPC5_NSLOT")) S = std::min(kMaxSlots, std::max(2, atoi(e)));
+    // 4 warps per CTA: with 168 registers per thread three CTAs share an SM
+    // tuning knobs, read once per process: SPC5_WPC (warps per CTA), SPC5_NSLOT
+    static const int env_wpc = [] {
+        const char *e = getenv("SPC5_WPC");
+        return e ? std::min(8, std::max(1, atoi(e))) : 0;
+    }();
+    static const int env_nslot = [] {
+        const char *e = getenv("SPC5_NSLOT");
+        return e ? std::min(kMaxSlots, std::max(2, atoi(e))) : 2;
+    }();
+    int wpc = env_wpc ? env_wpc : 4;
+    const int S = env_nslot;
     a.nslot = S;
     const size_t smem = kRingOff + (size_t)wpc * S * a.lay_bytes;  // barriers + ring
     SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -254,10 +254,22 @@ def test_giant_panels_split_and_fixup(spc5):
                 assert yp.tobytes() == y.tobytes(), (prec, r, vs, w)
 
 
-def test_parallel_bitwise_equal(spc5):
+def _parallel_cases():
+    from paper_2307_14774_b200.workloads import fem_rows, powerlaw_rows
     for name in ("tall", "longrows", "rand07", "dense16", "lastpanel"):
         m = small_case(name)
-        x = case_x(name, m)
+        yield name, m, case_x(name, m)
+    # irregular rows (balanced-lane-range chunks) and dense 3x3 blocks
+    for name, m in (("powerlaw", powerlaw_rows(1000, 1400, precision="f64")),
+                    ("fem", fem_rows(3000, 3300))):
+        yield name, m, np.random.default_rng(7).uniform(-1, 1, m.num_cols)
+
+
+@pytest.mark.parametrize("lpr_split", [False, True])
+def test_parallel_bitwise_equal(spc5, lpr_split, monkeypatch):
+    if lpr_split:
+        monkeypatch.setenv("SPC5_LPR_SPLIT", "1")
+    for name, m, x in _parallel_cases():
         prec = "f32" if m.values.dtype == np.float32 else "f64"
         for r in (1, 2, 4, 8):
             s = spc5.csr_to_spc5(m, r, 8)
