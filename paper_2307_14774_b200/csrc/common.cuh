@@ -104,7 +104,11 @@ struct Mirror {
     double scale = 1.0;
 };
 int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void *y,
-                int accumulate, cudaStream_t st, const Mirror *mirror = nullptr);
+                int accumulate, cudaStream_t st, const Mirror *mirror = nullptr,
+                const int64_t *blk = nullptr);
+// host-buffer pipeline: K nnz-balanced panel stages, their block bounds and
+// the x prefix (columns) each stage reads
+int host_stages(const Matrix &m, int K, int64_t *p, int64_t *b, int64_t *need, cudaStream_t st);
 int partition_by_nnz(const Matrix &m, int workers, int64_t *h_ranges, cudaStream_t st);
 int block_value_offsets(const Matrix &m, int64_t *d_offsets, cudaStream_t st);
 int validate_structure(const Matrix &m, cudaStream_t st);

@@ -838,6 +838,60 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     return SPC5_OK;
 }
 
+// stage s of the host pipeline reads x columns < need[s]: per block, col + vs
+// (clipped), max over the stage's blocks
+__global__ void stage_need_kernel(int64_t nb, const uint32_t *__restrict__ colidx, int vs,
+                                  int64_t num_cols, const int64_t *__restrict__ bnd, int K,
+                                  unsigned long long *need) {
+    int64_t b = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    int best = -1, bs = 0;
+    for (; b < nb; b += (int64_t)gridDim.x * blockDim.x) {
+        int s = 0;
+        while (s + 1 < K && b >= bnd[s + 1]) ++s;
+        const int64_t e = min((int64_t)colidx[b] + vs, num_cols);
+        if (s != bs && best >= 0) {
+            atomicMax(need + bs, (unsigned long long)best);
+            best = -1;
+        }
+        bs = s;
+        best = max(best, (int)e);
+    }
+    if (best >= 0) atomicMax(need + bs, (unsigned long long)best);
+}
+
+int host_stages(const Matrix &m, int K, int64_t *p, int64_t *b, int64_t *need, cudaStream_t st) {
+    std::vector<int64_t> ranges(2 * K);
+    SPC5_TRY(partition_by_nnz(m, K, ranges.data(), st));
+    for (int k = 0; k < K; ++k) p[k] = ranges[2 * k];
+    p[K] = m.num_panels;
+    for (int k = 0; k <= K; ++k)
+        SPC5_CUDA(cudaMemcpyAsync(b + k, m.rowptr + p[k], sizeof(int64_t), cudaMemcpyDeviceToHost,
+                                  st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    int64_t *d_bnd = nullptr;
+    unsigned long long *d_need = nullptr;
+    SPC5_TRY(dev_alloc(&d_bnd, (size_t)K + 1));
+    SPC5_TRY(dev_alloc(&d_need, (size_t)K));
+    SPC5_CUDA(cudaMemcpyAsync(d_bnd, b, sizeof(int64_t) * (K + 1), cudaMemcpyHostToDevice, st));
+    SPC5_CUDA(cudaMemsetAsync(d_need, 0, sizeof(unsigned long long) * K, st));
+    if (m.num_blocks)
+        stage_need_kernel<<<(unsigned)std::min<int64_t>(cdiv(m.num_blocks, 256), 148 * 16), 256, 0,
+                            st>>>(m.num_blocks, m.colidx, m.vs, m.num_cols, d_bnd, K, d_need);
+    SPC5_CUDA(cudaGetLastError());
+    std::vector<unsigned long long> h(K);
+    SPC5_CUDA(cudaMemcpyAsync(h.data(), d_need, sizeof(unsigned long long) * K,
+                              cudaMemcpyDeviceToHost, st));
+    SPC5_CUDA(cudaStreamSynchronize(st));
+    dev_free(d_bnd);
+    dev_free(d_need);
+    int64_t run = 0;  // prefix max: stage k may start once x[0, need[k]) has landed
+    for (int k = 0; k < K; ++k) {
+        run = std::max<int64_t>(run, (int64_t)h[k]);
+        need[k] = run;
+    }
+    return SPC5_OK;
+}
+
 int partition_by_nnz(const Matrix &m, int workers, int64_t *h_ranges, cudaStream_t st) {
     if (workers < 1) return fail(SPC5_EINVAL, "workers must be >= 1");
     std::vector<int64_t> bounds(workers + 1, 0);

@@ -29,6 +29,9 @@
 //    bitwise reproducible across runs, spmv_parallel ranges and GPU shards.
 #include <algorithm>
 #include <cstdlib>
+#include <map>
+#include <mutex>
+#include <tuple>
 
 #include "common.cuh"
 
@@ -972,11 +975,24 @@ int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
     const int S = env_nslot;
     a.nslot = S;
     const size_t smem = kRingOff + (size_t)wpc * S * a.lay_bytes;  // barriers + ring
-    SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+    // launch shape per (kernel, warps, shared memory), computed once: the
+    // attribute/occupancy queries cost more host time than a launch
     int per_sm = 0;
-    SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, wpc * 32, smem));
-    if (per_sm < 1) per_sm = 1;
+    {
+        static std::mutex mu;
+        static std::map<std::tuple<const void *, int, size_t>, int> cache;
+        std::lock_guard<std::mutex> lk(mu);
+        const auto key = std::make_tuple((const void *)kernel, wpc, smem);
+        auto it = cache.find(key);
+        if (it == cache.end()) {
+            SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                           227 * 1024));
+            SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, wpc * 32,
+                                                                    smem));
+            it = cache.emplace(key, std::max(per_sm, 1)).first;
+        }
+        per_sm = it->second;
+    }
     int64_t grid = std::max<int64_t>(cdiv(std::max<int64_t>(nslots, 1), wpc),
                                      a.accumulate ? 1 : cdiv(a.num_empty, 256));
     grid = std::min<int64_t>(grid, (int64_t)m.sm_count * per_sm);
@@ -1017,7 +1033,7 @@ int dispatch_r(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
 }  // namespace
 
 int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void *y,
-                int accumulate, cudaStream_t st, const Mirror *mirror) {
+                int accumulate, cudaStream_t st, const Mirror *mirror, const int64_t *blk) {
     const Plan &P = m.plan;
     SpmvArgs a{};
     a.yscale = 1.0;
@@ -1062,9 +1078,16 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
         a.b_hi = m.num_blocks;
     } else {
         int64_t blo = 0, bhi = 0;
-        SPC5_CUDA(cudaMemcpyAsync(&blo, m.rowptr + p_lo, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SPC5_CUDA(cudaMemcpyAsync(&bhi, m.rowptr + p_hi, sizeof(int64_t), cudaMemcpyDeviceToHost, st));
-        SPC5_CUDA(cudaStreamSynchronize(st));
+        if (blk) {  // block range known to the caller: no round trip
+            blo = blk[0];
+            bhi = blk[1];
+        } else {
+            SPC5_CUDA(cudaMemcpyAsync(&blo, m.rowptr + p_lo, sizeof(int64_t),
+                                      cudaMemcpyDeviceToHost, st));
+            SPC5_CUDA(cudaMemcpyAsync(&bhi, m.rowptr + p_hi, sizeof(int64_t),
+                                      cudaMemcpyDeviceToHost, st));
+            SPC5_CUDA(cudaStreamSynchronize(st));
+        }
         a.b_lo = blo;
         a.b_hi = bhi;
         const int64_t *cb = P.h_chunk_b;
