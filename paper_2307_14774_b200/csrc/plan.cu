@@ -728,7 +728,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         dev_free(d_mx);
         P.split_len = sl;
     }
-    int64_t slot_cap = 10 * 1024;  // target ring-slot size (tuning knob SPC5_SLOT_KB)
+    // ring-slot size cap: 3 CTAs x 4 warps x 2 slots + 512 B each fit 228 KB
+    int64_t slot_cap = 9472;  // (tuning knob SPC5_SLOT_KB)
     if (const char *e = getenv("SPC5_SLOT_KB")) slot_cap = std::max(1, atoi(e)) * 1024;
     // lane-per-panel chunks: the longest panel times the panel count may exceed
     // the chunk's blocks by lpr_bal/4 (knob SPC5_LPR_BAL, quarters)
@@ -764,7 +765,11 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         // records: panel records (lane-per-panel chunks) or 32 lane records
         P.lay_col = P.lay_rp + a16(std::max<int64_t>(P.max_lpp_panels + 1, 32) * 4 + 32);
         P.lay_mask = P.lay_col + a16(mb * 4 + 32);
-        P.lay_val = P.lay_mask + a16(mb * m.r * m.mask_bytes() + 32);
+        // + slack: lane-per-panel-row steps (U <= 18 blocks for r = 8, <= 9
+        // otherwise) load up to U-1 blocks past a lane's range, masked off
+        // afterwards, without bounds checks
+        const int64_t lb = m.r * m.mask_bytes();
+        P.lay_val = P.lay_mask + a16(mb * lb + std::max<int64_t>(32, ((m.r == 8 ? 18 : 9) - 1) * lb));
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
                              128 * 128);
         if (P.slot_bytes <= slot_cap || cb == 1) break;

@@ -28,6 +28,7 @@
 //    summed in an order fixed by global block positions only, so results are
 //    bitwise reproducible across runs, spmv_parallel ranges and GPU shards.
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <map>
 #include <mutex>
@@ -75,7 +76,8 @@ struct SpmvArgs {
 constexpr unsigned kFull = 0xffffffffu;
 constexpr int kMaxSlots = 4;  // ring slots per warp (SpmvArgs::nslot)
 constexpr uint32_t kHdr = 64;  // slot header bytes (chunk descriptor)
-constexpr uint32_t kRingOff = 256;  // barriers (8 warps x kMaxSlots) before the ring
+constexpr uint32_t kRecOff = 256;   // per-warp staging of the next issue record (32 B)
+constexpr uint32_t kRingOff = 512;  // barriers (8 warps x kMaxSlots), records, then the ring
 
 // ---- TMA (cp.async.bulk) + mbarrier helpers -------------------------------
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
@@ -375,6 +377,26 @@ __device__ __forceinline__ void issue_chunk(const SpmvArgs &a, uint4 A, uint4 B,
     bulk_g2s(slot + a.lay_mask, maskb + (size_t)A.z * 16, (B.y & 0xffffu) * 16, bar, pol);
     if (B.y >> 16) bulk_g2s(slot + a.lay_val, valb + (size_t)A.w * 16, (B.y >> 16) * 16, bar, pol);
 }
+// The refill's issue record is prefetched into shared memory with cp.async
+// while the chunk is consumed (held in registers across the chunk it was
+// spilled to local memory, i.e. an L2 round trip at refill time).
+__device__ __forceinline__ void ir_prefetch(const SpmvArgs &a, int64_t c, uint32_t dst) {
+    asm volatile(
+        "cp.async.cg.shared.global [%0], [%1], 16;\n"
+        "cp.async.cg.shared.global [%2], [%3], 16;\n"
+        "cp.async.commit_group;\n" ::"r"(dst),
+        "l"(a.issue_rec + 2 * c), "r"(dst + 16u), "l"(a.issue_rec + 2 * c + 1)
+        : "memory");
+}
+__device__ __forceinline__ void ir_staged(uint32_t src, uint4 &A, uint4 &B) {
+    asm volatile("cp.async.wait_all;" ::: "memory");
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(A.x), "=r"(A.y), "=r"(A.z), "=r"(A.w)
+                 : "r"(src));
+    asm volatile("ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(B.x), "=r"(B.y), "=r"(B.z), "=r"(B.w)
+                 : "r"(src + 16u));
+}
 __device__ __forceinline__ void ir_load(const SpmvArgs &a, int64_t c, bool valid, uint4 &A,
                                         uint4 &B) {
     if (valid) {
@@ -472,6 +494,167 @@ __device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s
     }
 }
 
+// Pair slots (lane-per-panel-row steps): blocks 2i and 2i+1 of the lane's row
+// form one 2*BB-bit word, so a step costs max-over-lanes(bits of a PAIR)
+// slots instead of twice max-over-lanes(bits of a BLOCK) -- the row's bits
+// are often all in one block of the pair (beta(8,8) stencil: 3+0 / 2+1 / 1+2).
+// Bits highest first: the high block's (storage-later) bits, then the low
+// block's; every product is accumulated in that fixed order.
+template <typename T, int UP, int NS, int BB>
+__device__ __forceinline__ void pair_slots(double &acc, const uint32_t (&m)[2 * UP],
+                                           const int (&h)[2 * UP], const T *__restrict__ x,
+                                           const uint32_t (&col)[2 * UP],
+                                           const uint32_t (&vaddr)[2 * UP]) {
+    constexpr uint32_t SZ = (uint32_t)sizeof(T);
+    T xv[UP][NS];
+    uint32_t P[UP], vhi[UP], vlo[UP];
+    int c[UP], hh[UP];
+#pragma unroll
+    for (int i = 0; i < UP; ++i) {
+        P[i] = m[2 * i] | (m[2 * i + 1] << BB);
+        hh[i] = h[2 * i + 1];
+        c[i] = h[2 * i] + hh[i];
+        // slot u of the pair reads vhi - u (u < hh) or vlo - u (low block)
+        vhi[i] = vaddr[2 * i + 1] + (uint32_t)(hh[i] - 1) * SZ;
+        vlo[i] = vaddr[2 * i] + (uint32_t)(c[i] - 1) * SZ;
+    }
+#pragma unroll
+    for (int u = 0; u < NS; ++u) {
+#pragma unroll
+        for (int i = 0; i < UP; ++i) {
+            const uint32_t pos = bfind(P[i]);
+            P[i] &= ~(1u << pos);
+            const uint32_t xi = pos >= (uint32_t)BB ? col[2 * i + 1] + pos - BB : col[2 * i] + pos;
+            xv[i][u] = ldg_pred(x + xi, u < c[i]);
+        }
+    }
+#pragma unroll
+    for (int i = 0; i < UP; ++i) {
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+            const uint32_t va = (u < hh[i] ? vhi[i] : vlo[i]) - (uint32_t)u * SZ;
+            mac<T>(acc, lds_pred<T>(va, u < c[i]), xv[i][u]);
+        }
+    }
+}
+
+__device__ __forceinline__ uint32_t lds_mask_row(uint32_t addr, int mb) {
+    uint32_t v;
+    if (mb == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
+    else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
+    return v;
+}
+
+// Lane-per-panel-row steps, v2.  A lane loads only its own row's mask of each
+// block (immediate offsets from the step base; blocks past its range are
+// masked to 0).  Value offsets come from the per-block bit counts h packed
+// FB bits per block into words: an exclusive scan of the words over the R
+// row-lanes of the panel (shfl.up by G) gives the bits of the rows below,
+// the last row-lane's inclusive word gives the block totals, and one
+// multiply gives their exclusive prefix over the word's blocks.  No lane
+// popcounts the other rows' masks.  Field widths: FB=8 (vs<=8: h<=8, sums
+// over 8 rows <= 64, prefix of 3 totals + rows below <= 248) or FB=16.
+// PAIRS (U even): steps whose pair slots beat block slots use pair_slots.
+#ifndef SPC5_LPP2
+#define SPC5_LPP2 1
+#endif
+template <typename T, typename MT, int R, int U, bool PAIRS>
+__device__ __forceinline__ void lpp_steps2(double &acc, int maxlen, int my, int s, int rr, int lg,
+                                           int lane, uint32_t vaddr, uint32_t a_col,
+                                           uint32_t a_mask, const T *__restrict__ x) {
+    constexpr int MB = (int)sizeof(MT);
+    constexpr int LB = R * MB;
+    constexpr int FB = MB == 1 ? 8 : 16;
+    constexpr int BPW = 32 / FB;
+    constexpr int NW = (U + BPW - 1) / BPW;
+    constexpr uint32_t FM = FB == 8 ? 0xffu : 0xffffu;
+    constexpr uint32_t SZ = (uint32_t)sizeof(T);
+    const int width = R << lg;
+    const int src_last = (lane & ~(width - 1)) | ((R - 1) << lg) | (lane & ((1 << lg) - 1));
+    const uint32_t own = (uint32_t)(rr * MB);
+    for (int j = 0; j < maxlen; j += U) {
+        const int rem = my - j;
+        const uint32_t bj = (uint32_t)(rem > 0 ? s + j : s);
+        const uint32_t cb = a_col + bj * 4u, mbase = a_mask + bj * (uint32_t)LB + own;
+        uint32_t col[U], m[U], vr[U];
+        int h[U];
+        uint32_t H[NW];
+#pragma unroll
+        for (int w = 0; w < NW; ++w) H[w] = 0u;
+#pragma unroll
+        for (int k = 0; k < U; ++k) {
+            col[k] = lds_u32(cb + (uint32_t)k * 4u);
+            const uint32_t raw = lds_mask_row(mbase + (uint32_t)(k * LB), MB);
+            m[k] = k < rem ? raw : 0u;
+            h[k] = __popc(m[k]);
+            H[k / BPW] |= (uint32_t)h[k] << (FB * (k % BPW));
+        }
+#pragma unroll
+        for (int w = 0; w < NW; ++w) {
+            uint32_t inc = H[w], tot = H[w];
+            if constexpr (R > 1) {
+#pragma unroll
+                for (int d = 1; d < R; d <<= 1) {
+                    const uint32_t t = __shfl_up_sync(kFull, inc, d << lg, width);
+                    if (rr >= d) inc += t;
+                }
+                tot = __shfl_sync(kFull, inc, src_last);
+            }
+            const uint32_t ep = FB == 8 ? tot * 0x01010100u : tot << 16;  // exclusive prefix
+            const uint32_t vw = ep + (inc - H[w]);  // + rows below, per field
+#pragma unroll
+            for (int i = 0; i < BPW; ++i) {
+                const int k = w * BPW + i;
+                if (k < U) vr[k] = vaddr + ((vw >> (FB * i)) & FM) * SZ;
+            }
+            vaddr += ((ep >> (32 - FB)) + (tot >> (32 - FB))) * SZ;  // the word's values
+        }
+        int cm = 0;
+#pragma unroll
+        for (int k = 0; k < U; ++k) cm = max(cm, h[k]);
+        const int cmax = __reduce_max_sync(kFull, cm);
+        if constexpr (PAIRS && U % 2 == 0) {
+            int cp = 0;
+#pragma unroll
+            for (int i = 0; i < U / 2; ++i) cp = max(cp, h[2 * i] + h[2 * i + 1]);
+            const int cpmax = __reduce_max_sync(kFull, cp);
+            // pair slots cost ~13 instructions, block slots ~11
+            if (cpmax <= 3 && cpmax * 13 < cmax * 22) {
+                if (cpmax == 1) pair_slots<T, U / 2, 1, 8 * MB>(acc, m, h, x, col, vr);
+                else if (cpmax == 2) pair_slots<T, U / 2, 2, 8 * MB>(acc, m, h, x, col, vr);
+                else pair_slots<T, U / 2, 3, 8 * MB>(acc, m, h, x, col, vr);
+                continue;
+            }
+        }
+        if constexpr (U <= 9) {
+            uint32_t mm[U];
+            int hh[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                mm[k] = m[k];
+                hh[k] = h[k];
+            }
+            row_dispatch<T, U>(acc, mm, hh, x, col, vr, cmax);
+        } else {  // two halves (register budget of the gathers in flight)
+            constexpr int U1 = U / 2, U2 = U - U / 2;
+            uint32_t m1[U1], c1[U1], v1[U1], m2[U2], c2[U2], v2[U2];
+            int h1[U1], h2[U2], cm1 = 0, cm2 = 0;
+#pragma unroll
+            for (int k = 0; k < U1; ++k) {
+                m1[k] = m[k]; c1[k] = col[k]; v1[k] = vr[k]; h1[k] = h[k];
+                cm1 = max(cm1, h[k]);
+            }
+#pragma unroll
+            for (int k = 0; k < U2; ++k) {
+                m2[k] = m[U1 + k]; c2[k] = col[U1 + k]; v2[k] = vr[U1 + k]; h2[k] = h[U1 + k];
+                cm2 = max(cm2, h[U1 + k]);
+            }
+            row_dispatch<T, U1>(acc, m1, h1, x, c1, v1, __reduce_max_sync(kFull, cm1));
+            row_dispatch<T, U2>(acc, m2, h2, x, c2, v2, __reduce_max_sync(kFull, cm2));
+        }
+    }
+}
+
 template <typename T, typename MT, int R, bool GENERIC>
 __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int npc,
                                           int lg, bool head_mid, uint32_t a_zero, uint32_t a_rec,
@@ -502,12 +685,30 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t 
         // U blocks per step (U from the longest lane range): all their x
         // gathers are in flight before the first FMA; values still accumulate
         // in storage order
-        if (maxlen <= 3) {
-            lpp_steps<T, MT, R, 3>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
-        } else if (maxlen <= 6) {
-            lpp_steps<T, MT, R, 6>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
+        if (!SPC5_LPP2) {
+            if (maxlen <= 3) {
+                lpp_steps<T, MT, R, 3>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
+            } else if (maxlen <= 6) {
+                lpp_steps<T, MT, R, 6>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
+            } else {
+                lpp_steps<T, MT, R, 9>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
+            }
+        } else if constexpr (R == 8) {  // pair slots: steps of 6 / 12 / 18 blocks
+            if (maxlen <= 6) {
+                lpp_steps2<T, MT, R, 6, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+            } else if (maxlen <= 12) {
+                lpp_steps2<T, MT, R, 12, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+            } else {
+                lpp_steps2<T, MT, R, 18, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+            }
         } else {
-            lpp_steps<T, MT, R, 9>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
+            if (maxlen <= 3) {
+                lpp_steps2<T, MT, R, 3, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+            } else if (maxlen <= 6) {
+                lpp_steps2<T, MT, R, 6, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+            } else {
+                lpp_steps2<T, MT, R, 9, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+            }
         }
         for (int o = 1; o < G; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
         const int64_t p = p0 + q;
@@ -873,9 +1074,9 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
     uint32_t parity = 0;
     for (int64_t c = cfirst; c < c_end; c += stride) {
         const int64_t cn = c + S * stride;  // the chunk that refills this slot
-        // its issue record: loaded now, the latency hides behind this chunk's work
-        uint4 nA, nB;
-        ir_load(a, cn, lane == 0 && cn < c_end, nA, nB);
+        // its issue record: prefetched now, the latency hides behind this chunk's work
+        const uint32_t rec_stage = smem_addr(smem) + kRecOff + (uint32_t)warp * 32u;
+        if (lane == 0 && cn < c_end) ir_prefetch(a, cn, rec_stage);
         const uint32_t sbase = ring + (uint32_t)slot_i * a.lay_bytes;
         mbar_wait(bars + slot_i, parity);
         // this chunk's descriptor, written into the slot header by the producer
@@ -914,6 +1115,8 @@ __global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
         // ---- release the slot and refill it with the chunk S ahead
         __syncwarp();
         if (lane == 0 && cn < c_end) {
+            uint4 nA, nB;
+            ir_staged(rec_stage, nA, nB);
             asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
             issue_chunk<T, LB>(a, nA, nB, sbase, bars + slot_i, pol);
         }
@@ -990,6 +1193,9 @@ int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
             SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, wpc * 32,
                                                                     smem));
             it = cache.emplace(key, std::max(per_sm, 1)).first;
+            if (getenv("SPC5_PLAN_DEBUG"))
+                fprintf(stderr, "spc5 launch: %d warps/CTA, %zu B shared, %d CTAs/SM\n", wpc,
+                        smem, per_sm);
         }
         per_sm = it->second;
     }
