@@ -12,7 +12,9 @@ from . import _native  # noqa: F401  (loads libspc5_b200.so, raises ImportError 
 from .blocks import (VALID_R, VALID_VS, FillingStats, Spc5Matrix, csr_to_spc5,
                      csr_to_spc5_device, filling_stats, footprint_comparison, load_spc5,
                      mask_dtype, save_spc5, spc5_to_csr, validate_spc5)
-from .harness import BenchRecord, ValidationError, run_bench, run_kernel
+from .harness import (CSV_VERSION_LINE, BenchRecord, CostModelFit, InsufficientDataError,
+                      ValidationError, fit_cost_model, read_records, run_bench, run_kernel,
+                      spearman_rank_correlation, write_records, write_scatter)
 from .kernels import (KernelConfig, SpmvResult, VerifyReport, block_value_offsets,
                       csr_reference, mask_popcounts, spmv, spmv_spc5_scalar, spmv_spc5_vector,
                       verify_against_oracle)
@@ -22,6 +24,8 @@ from .parallel import Partition, partition_by_nnz, spmv_parallel
 __version__ = "0.1.0"
 
 __all__ = [
+    "CSV_VERSION_LINE", "CostModelFit", "InsufficientDataError", "fit_cost_model",
+    "read_records", "spearman_rank_correlation", "write_records", "write_scatter",
     "BenchRecord", "CsrMatrix", "FillingStats", "KernelConfig", "Partition", "Spc5Matrix",
     "SpmvResult", "VALID_R", "VALID_VS", "ValidationError", "VerifyReport",
     "block_value_offsets", "csr_reference", "csr_to_spc5", "csr_to_spc5_device",

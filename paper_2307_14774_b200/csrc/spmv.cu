@@ -71,6 +71,7 @@ struct SpmvArgs {
     int nmirror;
     int64_t mirror_row0;
     double yscale;
+    int plain;  // !accumulate && !nmirror && yscale == 1
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -230,6 +231,10 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 // one y row: y[row] (+)= v, mirrored to the peer buffers of the fused exchange
 template <typename T>
 __device__ __forceinline__ void put_row(const SpmvArgs &a, T *y, int64_t row, double v) {
+    if (a.plain) {  // y = A.x, no mirrors: one store (a uniform branch, not predication)
+        y[row] = (T)v;
+        return;
+    }
     T sv = (T)(v * a.yscale);
     if (a.accumulate) sv = y[row] + sv;
     y[row] = sv;
@@ -1310,6 +1315,7 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
             return SPC5_OK;
         }
     }
+    a.plain = !accumulate && a.nmirror == 0 && a.yscale == 1.0;
     const bool f64 = m.precision == SPC5_F64;
     const bool wide = m.vs > 8;
     if (f64) return wide ? dispatch_r<double, uint16_t>(m, a, st) : dispatch_r<double, uint8_t>(m, a, st);
