@@ -214,9 +214,22 @@ def cpu_product_sample(cfg_id, formats, budget_s=15.0, threads=None):
 
     Returns (gflops, cores, sample description, per-format y for parity)."""
     from oracle import oracle
-    from paper_2307_14774_b200.workloads import CONFIGS, config1, stencil27, x_vector
+    from paper_2307_14774_b200.workloads import (CONFIGS, config1, fem_rows, powerlaw_rows,
+                                                 stencil27, stencil27_rows, x_vector)
     cfg = CONFIGS[cfg_id]
-    m = config1() if cfg_id == 1 else stencil27(cfg["n"], cfg["precision"])
+    # configs 1-2: the whole matrix; 3-5: the first rows (~4 M nnz, a multiple of
+    # every r): conversion and product are panel-local, so the slice's y is
+    # the full product's y[:hi] (SURVEY 8(c) sliced oracle)
+    if cfg_id == 1:
+        m = config1()
+    elif cfg_id == 2:
+        m = stencil27(cfg["n"], cfg["precision"])
+    elif cfg.get("gen") == "powerlaw":
+        m = powerlaw_rows(0, 262_144)
+    elif cfg.get("gen") == "fem":
+        m = fem_rows(0, 49_152)
+    else:
+        m = stencil27_rows(cfg["n"], 0, 147_456, cfg["precision"])
     x = x_vector(m.num_cols, cfg["precision"])
     threads = threads or oracle.threads()
     flops, secs, reps_total, ys = 0.0, 0.0, 0, {}
@@ -235,7 +248,8 @@ def cpu_product_sample(cfg_id, formats, budget_s=15.0, threads=None):
         flops += 2.0 * m.nnz * reps
         secs += t_f
         reps_total += reps
-    sample = (f"config {cfg_id}: full products, {reps_total} total over formats "
+    what = "full products" if cfg_id <= 2 else f"products of rows [0, {m.num_rows})"
+    sample = (f"config {cfg_id}: {what}, {reps_total} total over formats "
               f"{[fmt_key(*f) for f in formats]}, C port of kernels.py:121-143, "
               f"{threads} OpenMP threads")
     return flops / secs / 1e9, threads, sample, ys, m, x
@@ -423,7 +437,8 @@ def ours_single(args, formats):
         _, abs_ref = oracle.csr_reference(m_host, x_host)
         parity = {}
         for f in formats:
-            err = oracle.relative_error(ys[f].cpu().numpy(), cpu_ys[f], abs_ref)
+            err = oracle.relative_error(ys[f].cpu().numpy()[:m_host.num_rows], cpu_ys[f],
+                                        abs_ref)
             parity[fmt_key(*f)] = float(err.max())
         cpu = {"value": gfl, "unit": "GFLOP/s", "cores": cores, "kind": "port",
                "sample": sample, "max_rel_err_gpu_vs_cpu": parity}

@@ -711,8 +711,14 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         const int64_t per_block = 4 + m.r * m.mask_bytes();
         int64_t win_cap = 6 * 1024;  // bytes of the fullest split window (knob SPC5_WIN_KB)
         if (const char *e = getenv("SPC5_WIN_KB")) win_cap = std::max(1, atoi(e)) * 1024;
-        int64_t sl = 512;
-        for (; sl > 1; sl >>= 1) {
+        // candidates: powers of two and their 3/4 (a panel of 85 blocks is
+        // not cut at 96; any integer works for the global-multiple rule)
+        static const int64_t kSl[] = {512, 384, 256, 192, 128, 96, 64, 48, 32, 24, 16,
+                                      12, 8, 6, 4, 3, 2, 1};
+        int64_t sl = 1;
+        for (int64_t cand : kSl) {
+            sl = cand;
+            if (sl == 1) break;
             if (sl * per_block > win_cap) continue;
             unsigned long long h_mx = 0;
             SPC5_CUDA(cudaMemsetAsync(d_mx, 0, sizeof(unsigned long long), st));

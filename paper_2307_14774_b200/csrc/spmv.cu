@@ -250,6 +250,24 @@ __device__ __forceinline__ void store_rows(const SpmvArgs &a, T *y, int64_t row0
     }
 }
 
+// A warp-uniform slot count compared through an opaque register copy: keeps
+// the compiler from turning the dispatch if-chains into a jump table (BRX
+// through the constant bank, a long branch-resolution stall per step).
+#ifndef SPC5_NO_BRX
+#define SPC5_NO_BRX 1
+#endif
+__device__ __forceinline__ bool ueq(int v, int k) {
+#if SPC5_NO_BRX
+    int r;
+    asm volatile("{\n .reg .pred q;\n setp.eq.s32 q, %1, %2;\n selp.s32 %0, 1, 0, q;\n}"
+                 : "=r"(r)
+                 : "r"(v), "r"(k));
+    return r != 0;
+#else
+    return v == k;
+#endif
+}
+
 // Products of one panel row for U blocks: up to NS set bits per block,
 // highest first.  All U*NS gathers are issued before the first FMA; products
 // are accumulated block by block (storage order).  Slots past a block's count
@@ -294,13 +312,13 @@ __device__ __forceinline__ void row_dispatch(double &acc, uint32_t (&m)[U], int 
                                              const T *__restrict__ x, const uint32_t (&col)[U],
                                              const uint32_t (&vaddr)[U], int cmax) {
     if (cmax <= 0) return;
-    if (cmax == 1) {
+    if (ueq(cmax, 1)) {
         row_slots<T, U, 1>(acc, m, h, x, col, vaddr);
-    } else if (cmax == 2) {
+    } else if (ueq(cmax, 2)) {
         row_slots<T, U, 2>(acc, m, h, x, col, vaddr);
-    } else if (cmax == 3) {
+    } else if (ueq(cmax, 3)) {
         row_slots<T, U, 3>(acc, m, h, x, col, vaddr);
-    } else if (cmax == 4) {
+    } else if (ueq(cmax, 4)) {
         row_slots<T, U, 4>(acc, m, h, x, col, vaddr);
     } else {  // dense rows: one block at a time so the products stay in order
 #pragma unroll
@@ -353,11 +371,11 @@ __device__ __forceinline__ void row_dispatch_sep(double (&acc)[U], uint32_t (&m)
                                                  const uint32_t (&col)[U],
                                                  const uint32_t (&vaddr)[U], int cmax) {
     if (cmax <= 0) return;
-    if (cmax == 1) {
+    if (ueq(cmax, 1)) {
         row_slots_sep<T, U, 1>(acc, m, h, x, col, vaddr);
-    } else if (cmax == 2) {
+    } else if (ueq(cmax, 2)) {
         row_slots_sep<T, U, 2>(acc, m, h, x, col, vaddr);
-    } else if (cmax == 3) {
+    } else if (ueq(cmax, 3)) {
         row_slots_sep<T, U, 3>(acc, m, h, x, col, vaddr);
     } else {
         for (int done = 0; done < cmax; done += 4) row_slots_sep<T, U, 4>(acc, m, h, x, col, vaddr);
@@ -968,22 +986,47 @@ __device__ __forceinline__ void blr_chunk(const SpmvArgs &a, int64_t c, int64_t 
 #pragma unroll
             for (int k = 0; k < U; ++k) part[k][g] = pg[k];
         }
+        if (R == 1 && a.plain) {
+            // Branch-free closes (r = 1; for r > 1 the R predicated stores
+            // and selects per block cost more than the branch): a block that starts a panel stores the
+            // current one (predicated) or, the first time in a lane that
+            // began inside a panel, parks it in F.  The chunk's head panel
+            // of a split chunk is always closed through F (its first close
+            // in any lane), so no carry slot is written here.
+            T *yp = y + (p0 + p) * R;
 #pragma unroll
-        for (int k = 0; k < U; ++k) {
-            if (st[k]) {  // block starts a new panel: close the current one
-                if (!flushed && first_open) {
+            for (int k = 0; k < U; ++k) {
+                const bool toF = st[k] && !flushed && first_open;
+                const bool put = st[k] && !toF &&
+                                 (!GENERIC || (p0 + p >= a.p_lo && p0 + p < a.p_hi));
 #pragma unroll
-                    for (int g = 0; g < R; ++g) F[g] = acc[g];
-                } else {
-                    blr_put<T, R>(a, c, p0, p, head_mid, acc, y, GENERIC);
+                for (int g = 0; g < R; ++g) {
+                    F[g] = toF ? acc[g] : F[g];
+                    if (put && (R == 1 || (p0 + p) * R + g < a.num_rows)) yp[g] = (T)acc[g];
+                    acc[g] = st[k] ? part[k][g] : acc[g] + part[k][g];
                 }
-                flushed = true;
-                ++p;
-#pragma unroll
-                for (int g = 0; g < R; ++g) acc[g] = 0.0;
+                flushed |= st[k];
+                p += st[k] ? 1 : 0;
+                yp += st[k] ? R : 0;
             }
+        } else {
 #pragma unroll
-            for (int g = 0; g < R; ++g) acc[g] += part[k][g];
+            for (int k = 0; k < U; ++k) {
+                if (st[k]) {  // block starts a new panel: close the current one
+                    if (!flushed && first_open) {
+#pragma unroll
+                        for (int g = 0; g < R; ++g) F[g] = acc[g];
+                    } else {
+                        blr_put<T, R>(a, c, p0, p, head_mid, acc, y, GENERIC);
+                    }
+                    flushed = true;
+                    ++p;
+#pragma unroll
+                    for (int g = 0; g < R; ++g) acc[g] = 0.0;
+                }
+#pragma unroll
+                for (int g = 0; g < R; ++g) acc[g] += part[k][g];
+            }
         }
     }
     // join the panels that span lanes: segmented inclusive scan of L = acc

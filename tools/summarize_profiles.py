@@ -1,6 +1,6 @@
 """Summarise the ncu launch list and the full capture into profiles/ (round-tagged).
 
-usage: python tools/summarize_profiles.py ROUND LAUNCH_CSV FULL_REP
+usage: python tools/summarize_profiles.py ROUND LAUNCH_CSV FULL_REP[,FULL_REP...]
 Writes profiles/launches_<round>.csv (kernel, launches, total us, share),
 profiles/ncu_<round>.csv (key counters per captured K2 launch) and
 profiles/traffic.json (dram bytes per K2 launch, read by bench.py).
@@ -29,9 +29,15 @@ with open(out / f"launches_{rnd}.csv", "w") as f:
     w.writerow(["kernel", "block", "grid", "launches", "total_us", "mean_us", "share"])
     for (name, blk, grid), (n, t) in agg.items():
         w.writerow([name, blk, grid, n, f"{t:.1f}", f"{t / n:.1f}", f"{t / tot:.3f}"])
-raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
-                     text=True).stdout
-rr = list(csv.reader(io.StringIO(raw)))
+rr = []
+for one in rep.split(","):  # one capture per format, rows concatenated
+    raw = subprocess.run(["ncu", "-i", one, "--page", "raw", "--csv"], capture_output=True,
+                         text=True).stdout
+    part = list(csv.reader(io.StringIO(raw)))
+    if not rr:
+        rr = part
+    else:
+        rr += part[2:]
 hdr, units = rr[0], rr[1]
 want = ["Kernel Name", "gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
         "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed",
