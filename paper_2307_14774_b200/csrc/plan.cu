@@ -741,7 +741,11 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     // the chunk's blocks by lpr_bal/4 (knob SPC5_LPR_BAL, quarters)
     int lpr_bal = 4;
     if (const char *e = getenv("SPC5_LPR_BAL")) lpr_bal = std::max(4, atoi(e));
-    for (int64_t cb = 512;; cb >>= 1) {
+    // small matrices: chunks small enough that every resident warp of the
+    // GPU (SMs x 12) gets about one, so a product is one chunk deep
+    int64_t cb_max = 512;
+    while (cb_max > 32 && nb / cb_max < (int64_t)m.sm_count * 12) cb_max >>= 1;
+    for (int64_t cb = cb_max;; cb >>= 1) {
         SPC5_TRY(build_chunks(m, cb, st));
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
