@@ -20,11 +20,14 @@ e2e     the same products through the public API (paper_2307_14774_b200.spmv)
 cpu_baseline  the C restatement of the reference scalar kernel
         (oracle/spc5_oracle.c, kernels.py:121-143) on all host threads.
 
-N > 1 (torchrun): the config is split into nnz-balanced row-panel shards
-(partition_by_nnz); each rank converts only its rows and one step is one
-iterated product x <- A.x with the y-slices all-gathered into the next x over
-NCCL (strong scaling).  --impl reference runs the CPU port on
-rank 0 only; the other ranks exit 0.
+N > 1 (torchrun): weak scaling by default -- the stencil on an
+128 x 128 x (128 N) box, split into nnz-balanced row-panel shards
+(partition_by_nnz), i.e. one 128^3 cube of rows per GPU; each rank converts
+only its rows and one step is one product per format with x replicated and no
+data-path collective.  --scaling strong splits the config's one matrix (the
+default for config 5, BASELINE's multi-GPU config).  The iterated form x <-
+A.x with the y-slices all-gathered over NCCL is reported beside
+it.  --impl reference runs the CPU port on rank 0 only; the other ranks exit 0.
 """
 
 from __future__ import annotations
@@ -446,7 +449,9 @@ def ours_single(args, formats):
     line = {"metric": "SpMV GFLOP/s (2*nnz/t)", "value": value, "unit": "GFLOP/s",
             "n_gpus": 1, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": elapsed / args.steps * 1e3, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": prec, "data": "synthetic",
+            # --gpus N runs one n^3 cube of rows per GPU for config 2 (weak)
+            "scaling": args.scaling, "vs_baseline": None, "dtype": prec,
+            "data": "synthetic",
             "config": {"workload": cfgd["name"], "formats": [fmt_key(*f) for f in formats],
                        "num_rows": num_rows,
                        "nnz": mats[formats[0]].nnz,
@@ -469,7 +474,12 @@ def main():
     ap.add_argument("--formats", default=None, help="e.g. 1,8;2,8")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", choices=["weak", "strong"], default=None,
+                    help="N > 1: weak = one n^3 stencil cube per GPU (default, config 2); "
+                         "strong = the config's one matrix split over the GPUs (config 5)")
     args = ap.parse_args()
+    if args.scaling is None:
+        args.scaling = "weak" if args.config == 2 else "strong"
     if args.warmup < 3:
         args.warmup = 3
     from paper_2307_14774_b200.workloads import CONFIGS

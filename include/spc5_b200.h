@@ -183,6 +183,17 @@ int spc5_gen_stencil27_rowptr(int64_t n, int64_t row_lo, int64_t row_hi, int64_t
 int spc5_gen_stencil27_fill(int64_t n, int64_t row_lo, int64_t row_hi, int precision,
                             uint64_t seed, double diag, const int64_t *d_row_ptr,
                             int32_t *d_col_idx, void *d_values, void *stream);
+/*
+ * The same stencil on an n x n x nz box (nz = n is the cube above): the
+ * weak-scaling workload of bench.py --gpus N, where rank k owns z-slab k of an
+ * n x n x (n * N) box, i.e. one config-2 cube of rows per GPU.
+ */
+int spc5_gen_stencil27_box_rowptr(int64_t n, int64_t nz, int64_t row_lo, int64_t row_hi,
+                                  int64_t *d_row_ptr, void *stream);
+int spc5_gen_stencil27_box_fill(int64_t n, int64_t nz, int64_t row_lo, int64_t row_hi,
+                                int precision, uint64_t seed, double diag,
+                                const int64_t *d_row_ptr, int32_t *d_col_idx, void *d_values,
+                                void *stream);
 
 /*
  * Workload generator, BASELINE config 3: rows [row_lo, row_hi) of the n x n

@@ -57,6 +57,9 @@ SIGNATURES = {
     "spc5_gen_stencil27_rowptr": [_i64, _i64, _i64, _vp, _vp],
     "spc5_gen_stencil27_fill": [_i64, _i64, _i64, _int, ctypes.c_uint64, ctypes.c_double, _vp,
                                 _vp, _vp, _vp],
+    "spc5_gen_stencil27_box_rowptr": [_i64, _i64, _i64, _i64, _vp, _vp],
+    "spc5_gen_stencil27_box_fill": [_i64, _i64, _i64, _i64, _int, ctypes.c_uint64,
+                                    ctypes.c_double, _vp, _vp, _vp, _vp],
     "spc5_spmv_mirrored": [_H, _vp, _vp, ctypes.c_double, _vp, _int, _i64, _vp],
     "spc5_gen_powerlaw_rowptr": [_i64, _i64, _i64, ctypes.c_uint64, _vp, _int, _vp, _vp],
     "spc5_gen_powerlaw_fill": [_i64, _i64, _i64, _int, ctypes.c_uint64, _vp, _int, _vp, _vp, _vp,

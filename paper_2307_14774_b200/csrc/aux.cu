@@ -33,16 +33,20 @@ __device__ __forceinline__ int axis_count(int64_t c, int64_t n) {
     return 1 + (c > 0) + (c < n - 1);
 }
 
-__global__ void stencil_count_kernel(int64_t n, int64_t lo, int64_t rows, int64_t *counts) {
+// n x n x nz grid (nz = n: the cube of configs 2 and 5; nz = n * ranks: the
+// weak-scaling box whose z-slabs are the ranks' shards)
+__global__ void stencil_count_kernel(int64_t n, int64_t nz, int64_t lo, int64_t rows,
+                                     int64_t *counts) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (t >= rows) return;
     const int64_t i = lo + t;
     const int64_t z = i / (n * n), y = (i / n) % n, x = i % n;
-    counts[t] = (int64_t)axis_count(z, n) * axis_count(y, n) * axis_count(x, n);
+    counts[t] = (int64_t)axis_count(z, nz) * axis_count(y, n) * axis_count(x, n);
 }
 
 template <typename T>
-__global__ void stencil_fill_kernel(int64_t n, int64_t lo, int64_t rows, uint64_t seedmix,
+__global__ void stencil_fill_kernel(int64_t n, int64_t nz, int64_t lo, int64_t rows,
+                                    uint64_t seedmix,
                                     double diag, const int64_t *__restrict__ row_ptr,
                                     int32_t *__restrict__ col, T *__restrict__ val) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
@@ -51,7 +55,7 @@ __global__ void stencil_fill_kernel(int64_t n, int64_t lo, int64_t rows, uint64_
     const int64_t z = i / (n * n), y = (i / n) % n, x = i % n;
     int64_t k = row_ptr[t];
     for (int dz = -1; dz <= 1; ++dz) {
-        if (z + dz < 0 || z + dz >= n) continue;
+        if (z + dz < 0 || z + dz >= nz) continue;
         for (int dy = -1; dy <= 1; ++dy) {
             if (y + dy < 0 || y + dy >= n) continue;
             for (int dx = -1; dx <= 1; ++dx) {
@@ -260,15 +264,16 @@ __global__ void csr_exact_kernel(int64_t num_rows, const int64_t *__restrict__ r
 
 }  // namespace
 
-int gen_stencil27_rowptr(int64_t n, int64_t lo, int64_t hi, int64_t *rp, cudaStream_t st) {
-    if (n < 1 || lo < 0 || hi < lo || hi > n * n * n)
-        return fail(SPC5_EINVAL, "stencil27: bad n / row range");
+int gen_stencil27_rowptr(int64_t n, int64_t nz, int64_t lo, int64_t hi, int64_t *rp,
+                         cudaStream_t st) {
+    if (n < 1 || nz < 1 || lo < 0 || hi < lo || hi > n * n * nz || n * n * nz > (1ll << 31))
+        return fail(SPC5_EINVAL, "stencil27: bad n / nz / row range");
     const int64_t rows = hi - lo;
     SPC5_CUDA(cudaMemsetAsync(rp, 0, sizeof(int64_t), st));
     if (!rows) return SPC5_OK;
     int64_t *counts = nullptr;
     SPC5_TRY(dev_alloc(&counts, (size_t)rows));
-    stencil_count_kernel<<<(unsigned)cdiv(rows, 256), 256, 0, st>>>(n, lo, rows, counts);
+    stencil_count_kernel<<<(unsigned)cdiv(rows, 256), 256, 0, st>>>(n, nz, lo, rows, counts);
     SPC5_CUDA(cudaGetLastError());
     SPC5_TRY(scan_inclusive_i64(counts, rp + 1, rows, st));
     SPC5_CUDA(cudaStreamSynchronize(st));
@@ -276,17 +281,18 @@ int gen_stencil27_rowptr(int64_t n, int64_t lo, int64_t hi, int64_t *rp, cudaStr
     return SPC5_OK;
 }
 
-int gen_stencil27_fill(int64_t n, int64_t lo, int64_t hi, int precision, uint64_t seed,
-                       double diag, const int64_t *rp, int32_t *ci, void *v, cudaStream_t st) {
+int gen_stencil27_fill(int64_t n, int64_t nz, int64_t lo, int64_t hi, int precision,
+                       uint64_t seed, double diag, const int64_t *rp, int32_t *ci, void *v,
+                       cudaStream_t st) {
     const int64_t rows = hi - lo;
     if (rows <= 0) return SPC5_OK;
     const uint64_t seedmix = mix64_host(seed + 0x9E3779B97F4A7C15ull);
     const unsigned grid = (unsigned)cdiv(rows, 256);
     if (precision == SPC5_F64)
-        stencil_fill_kernel<double><<<grid, 256, 0, st>>>(n, lo, rows, seedmix, diag, rp, ci,
+        stencil_fill_kernel<double><<<grid, 256, 0, st>>>(n, nz, lo, rows, seedmix, diag, rp, ci,
                                                           static_cast<double *>(v));
     else
-        stencil_fill_kernel<float><<<grid, 256, 0, st>>>(n, lo, rows, seedmix, diag, rp, ci,
+        stencil_fill_kernel<float><<<grid, 256, 0, st>>>(n, nz, lo, rows, seedmix, diag, rp, ci,
                                                          static_cast<float *>(v));
     SPC5_CUDA(cudaGetLastError());
     return SPC5_OK;

@@ -456,16 +456,31 @@ int spc5_csr_exact(int64_t num_rows, int precision, const int64_t *d_row_ptr,
 
 int spc5_gen_stencil27_rowptr(int64_t n, int64_t row_lo, int64_t row_hi, int64_t *d_row_ptr,
                               void *stream) {
-    return gen_stencil27_rowptr(n, row_lo, row_hi, d_row_ptr, static_cast<cudaStream_t>(stream));
+    return gen_stencil27_rowptr(n, n, row_lo, row_hi, d_row_ptr,
+                                static_cast<cudaStream_t>(stream));
 }
 
 int spc5_gen_stencil27_fill(int64_t n, int64_t row_lo, int64_t row_hi, int precision,
                             uint64_t seed, double diag, const int64_t *d_row_ptr,
                             int32_t *d_col_idx, void *d_values, void *stream) {
+    return spc5_gen_stencil27_box_fill(n, n, row_lo, row_hi, precision, seed, diag, d_row_ptr,
+                                       d_col_idx, d_values, stream);
+}
+
+int spc5_gen_stencil27_box_rowptr(int64_t n, int64_t nz, int64_t row_lo, int64_t row_hi,
+                                  int64_t *d_row_ptr, void *stream) {
+    return gen_stencil27_rowptr(n, nz, row_lo, row_hi, d_row_ptr,
+                                static_cast<cudaStream_t>(stream));
+}
+
+int spc5_gen_stencil27_box_fill(int64_t n, int64_t nz, int64_t row_lo, int64_t row_hi,
+                                int precision, uint64_t seed, double diag,
+                                const int64_t *d_row_ptr, int32_t *d_col_idx, void *d_values,
+                                void *stream) {
     if (precision != SPC5_F32 && precision != SPC5_F64)
         return fail(SPC5_EINVAL, "precision must be 'f32' or 'f64'");
-    return gen_stencil27_fill(n, row_lo, row_hi, precision, seed, diag, d_row_ptr, d_col_idx,
-                              d_values, static_cast<cudaStream_t>(stream));
+    return gen_stencil27_fill(n, nz, row_lo, row_hi, precision, seed, diag, d_row_ptr,
+                              d_col_idx, d_values, static_cast<cudaStream_t>(stream));
 }
 
 int spc5_gen_powerlaw_rowptr(int64_t n, int64_t row_lo, int64_t row_hi, uint64_t seed,

@@ -116,7 +116,8 @@ int to_csr(const Matrix &m, int64_t *d_row_ptr, int32_t *d_col_idx, void *d_valu
            cudaStream_t st);
 int csr_exact(int64_t num_rows, int precision, const int64_t *rp, const int32_t *ci,
               const void *v, const void *x, double *y, double *a, cudaStream_t st);
-int gen_stencil27_rowptr(int64_t n, int64_t lo, int64_t hi, int64_t *rp, cudaStream_t st);
+int gen_stencil27_rowptr(int64_t n, int64_t nz, int64_t lo, int64_t hi, int64_t *rp,
+                         cudaStream_t st);
 int gen_powerlaw_rowptr(int64_t n, int64_t lo, int64_t hi, uint64_t seed, const int32_t *table,
                         int bits, int64_t *rp, cudaStream_t st);
 int gen_powerlaw_fill(int64_t n, int64_t lo, int64_t hi, int precision, uint64_t seed,
@@ -125,8 +126,9 @@ int gen_powerlaw_fill(int64_t n, int64_t lo, int64_t hi, int precision, uint64_t
 int gen_fem_rowptr(int64_t nodes, int64_t lo, int64_t hi, int64_t *rp, cudaStream_t st);
 int gen_fem_fill(int64_t nodes, int64_t lo, int64_t hi, int precision, uint64_t seed,
                  const int64_t *rp, int32_t *ci, void *v, cudaStream_t st);
-int gen_stencil27_fill(int64_t n, int64_t lo, int64_t hi, int precision, uint64_t seed,
-                       double diag, const int64_t *rp, int32_t *ci, void *v, cudaStream_t st);
+int gen_stencil27_fill(int64_t n, int64_t nz, int64_t lo, int64_t hi, int precision,
+                       uint64_t seed, double diag, const int64_t *rp, int32_t *ci, void *v,
+                       cudaStream_t st);
 
 // device allocation helpers (stream-ordered for temporaries)
 int dev_alloc(void **p, size_t bytes);

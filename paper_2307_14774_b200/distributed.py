@@ -185,8 +185,9 @@ def _shard_csr(cfg, lo, hi, prec):
     rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
     gen = cfg.get("gen", "stencil")
     table = torch.from_numpy(powerlaw_len_table()).to("cuda") if gen == "powerlaw" else None
+    nz = cfg.get("nz", cfg.get("n"))  # stencil box depth (weak scaling: n * ranks)
     if gen == "stencil":
-        nat.check(nat.lib.spc5_gen_stencil27_rowptr(cfg["n"], lo, hi, rp.data_ptr(), 0))
+        nat.check(nat.lib.spc5_gen_stencil27_box_rowptr(cfg["n"], nz, lo, hi, rp.data_ptr(), 0))
     elif gen == "powerlaw":
         nat.check(nat.lib.spc5_gen_powerlaw_rowptr(PL_N, lo, hi, 0, table.data_ptr(),
                                                    PL_TABLE_BITS, rp.data_ptr(), 0))
@@ -196,8 +197,9 @@ def _shard_csr(cfg, lo, hi, prec):
     ci = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
     va = torch.empty(max(nnz, 1), dtype=tdt, device="cuda")
     if gen == "stencil":
-        nat.check(nat.lib.spc5_gen_stencil27_fill(cfg["n"], lo, hi, pc, 0, 27.0, rp.data_ptr(),
-                                                  ci.data_ptr(), va.data_ptr(), 0))
+        nat.check(nat.lib.spc5_gen_stencil27_box_fill(cfg["n"], nz, lo, hi, pc, 0, 27.0,
+                                                      rp.data_ptr(), ci.data_ptr(),
+                                                      va.data_ptr(), 0))
     elif gen == "powerlaw":
         nat.check(nat.lib.spc5_gen_powerlaw_fill(PL_N, lo, hi, pc, 0, table.data_ptr(),
                                                  PL_TABLE_BITS, rp.data_ptr(), ci.data_ptr(),
@@ -212,14 +214,17 @@ def _shard_csr(cfg, lo, hi, prec):
 def bench_distributed(args, formats) -> None:
     """bench.py for N > 1 (one process per GPU, torchrun, NCCL).
 
-    The matrix's row panels are split nnz-balanced over the ranks
-    (panel_partition == partition_by_nnz); every rank converts only its rows.
-    One step = one product per format with x replicated and each rank writing
-    its own y-slice (no exchange needed: strong scaling of the same total
-    work as the 1-GPU line).  The iterated form (x <- A.x refreshed by the
-    NCCL all-gather of the y-slices, BASELINE config 5) is timed after it and
-    reported under "iterated".  Times are device times (CUDA events), the max
-    over ranks."""
+    --scaling weak (the default for config 2): the matrix is the 27-point
+    stencil on an n x n x (n * N) box, so every rank owns one n^3 cube of rows
+    (its z-slab) -- the 1-GPU line's work per GPU.  --scaling strong (the
+    default for config 5, BASELINE's multi-GPU config, and the only form for
+    configs 3/4) splits the config's one matrix.  Either way the row panels are split nnz-balanced
+    over the ranks (panel_partition == partition_by_nnz) and every rank
+    converts only its rows.  One step = one product per format with x
+    replicated and each rank writing its own y-slice: no data-path
+    collective.  The iterated form (x <- A.x refreshed by the NCCL all-gather
+    of the y-slices, BASELINE config 5) is timed after it and reported under
+    "iterated".  Times are device times (CUDA events), the max over ranks."""
     import json
     import os
     import time
@@ -241,10 +246,13 @@ def bench_distributed(args, formats) -> None:
     cfg = CONFIGS[args.config]
     if cfg.get("gen") is None and "n" not in cfg:
         raise SystemExit(f"config {args.config}: no device generator for the multi-GPU bench")
+    weak = "n" in cfg and getattr(args, "scaling", "weak") == "weak"
+    if weak:
+        cfg = dict(cfg, nz=cfg["n"] * world)
     prec = cfg["precision"]
     tdt = torch.float64 if prec == "f64" else torch.float32
     vb = 8 if prec == "f64" else 4
-    N = cfg["n"] ** 3 if "n" in cfg else cfg["rows"]
+    N = cfg["n"] ** 2 * cfg["nz"] if weak else cfg["rows"]
     C = N if "n" in cfg else cfg["cols"]
     # global row pointers (structure only) for the partition
     rp_all, ci_all, va_all = _shard_csr(cfg, 0, N, prec)
@@ -362,9 +370,12 @@ def bench_distributed(args, formats) -> None:
         line = {"metric": "SpMV GFLOP/s (2*nnz/t)", "value": flops * args.steps / tot_t / 1e9,
                 "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+                "higher_is_better": True, "scaling": "weak" if weak else "strong",
+                "vs_baseline": None,
                 "dtype": prec, "data": "synthetic",
-                "config": {"workload": cfg["name"], "formats": list(results),
+                "config": {"workload": (f"stencil27_{cfg['n']}x{cfg['n']}x{cfg['nz']}_{prec}"
+                                        f" ({cfg['n']}^3 rows per GPU)" if weak else cfg["name"]),
+                           "formats": list(results),
                            "num_rows": N, "nnz": results[next(iter(results))]["nnz"],
                            "step": "y_f = A_f.x for every format; x replicated, each rank "
                                    "writes its nnz-balanced row-panel slice of y",

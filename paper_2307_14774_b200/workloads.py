@@ -45,21 +45,24 @@ def keyed_uniform(i: np.ndarray, j: np.ndarray, seed: int) -> np.ndarray:
 
 
 def stencil27_rows(n: int, lo: int, hi: int, precision: str = "f64", seed: int = MATRIX_SEED,
-                   diag: float = 27.0) -> CsrMatrix:
-    """Rows [lo, hi) of the 27-point stencil on an n^3 grid, row = (z*n + y)*n + x.
+                   diag: float = 27.0, nz: int | None = None) -> CsrMatrix:
+    """Rows [lo, hi) of the 27-point stencil on an n x n x nz grid (nz = n: the
+    n^3 cube), row = (z*n + y)*n + x.
 
-    Returned as a CSR with ``hi - lo`` rows and ``n**3`` columns; the full
-    matrix is ``stencil27_rows(n, 0, n**3)``.
+    Returned as a CSR with ``hi - lo`` rows and ``n*n*nz`` columns; the full
+    matrix is ``stencil27_rows(n, 0, n**3)``.  Twin of csrc/aux.cu stencil_*
+    (``spc5_gen_stencil27[_box]_*``).
     """
     dtype = dtype_for(precision)
-    N = n ** 3
+    nz = n if nz is None else nz
+    N = n * n * nz
     lo, hi = max(0, lo), min(N, hi)
     i = np.arange(lo, hi, dtype=np.int64)
     z, y, x = i // (n * n), (i // n) % n, i % n
     cols = np.empty((len(i), 27), dtype=np.int64)
     valid = np.empty((len(i), 27), dtype=bool)
     for k, (dz, dy, dx) in enumerate(STENCIL27):
-        valid[:, k] = ((z + dz >= 0) & (z + dz < n) & (y + dy >= 0) & (y + dy < n)
+        valid[:, k] = ((z + dz >= 0) & (z + dz < nz) & (y + dy >= 0) & (y + dy < n)
                        & (x + dx >= 0) & (x + dx < n))
         cols[:, k] = i + dz * n * n + dy * n + dx
     counts = valid.sum(axis=1)

@@ -664,3 +664,28 @@ def test_lane_per_panel_row_steps(spc5, pattern):
                 oracle.spmv_spc5_scalar(oracle.csr_to_spc5(m, r, vs), x, y_ref)
                 assert_close(m, y, y_ref, x, f"{pattern} {np.dtype(dtype).name} {r},{vs}")
                 assert spc5.spmv(s, x).tobytes() == y.tobytes()
+
+
+def test_stencil_box_generator_matches_host(spc5):
+    """The weak-scaling box (n x n x nz, bench.py --gpus N): device rows ==
+    host twin rows, including slab edges whose columns reach the next slab."""
+    import torch
+
+    from paper_2307_14774_b200 import _native as nat
+    from paper_2307_14774_b200.workloads import stencil27_rows
+    n, nz = 10, 30
+    for prec, (lo, hi) in (("f64", (0, 300)), ("f32", (900, 1300)), ("f64", (2650, 3000))):
+        host = stencil27_rows(n, lo, hi, prec, nz=nz)
+        rp = torch.empty(hi - lo + 1, dtype=torch.int64, device="cuda")
+        nat.check(nat.lib.spc5_gen_stencil27_box_rowptr(n, nz, lo, hi, rp.data_ptr(), 0))
+        nnz = int(rp[-1])
+        ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
+        va = torch.empty(nnz, dtype=torch.float64 if prec == "f64" else torch.float32,
+                         device="cuda")
+        nat.check(nat.lib.spc5_gen_stencil27_box_fill(n, nz, lo, hi, 1 if prec == "f64" else 0,
+                                                      0, 27.0, rp.data_ptr(), ci.data_ptr(),
+                                                      va.data_ptr(), 0))
+        torch.cuda.synchronize()
+        assert np.array_equal(rp.cpu().numpy(), host.row_ptr)
+        assert np.array_equal(ci.cpu().numpy(), host.col_idx)
+        assert va.cpu().numpy().tobytes() == host.values.tobytes()

@@ -58,3 +58,23 @@ def test_fem_rows_shape():
     assert np.array_equal(m.col_idx[0:81], m.col_idx[81:162])
     v = fem_rows(0, 3000).values
     assert abs(float(v.mean())) < 0.02 and abs(float(v.std()) - 1.0) < 0.02
+
+
+def test_stencil_box_twin():
+    """n x n x nz box (weak scaling): nz = n is the cube; a slab's rows reach
+    the neighbouring slabs and interior rows keep all 27 entries."""
+    from paper_2307_14774_b200.workloads import stencil27_rows
+    n = 6
+    cube = stencil27_rows(n, 0, n ** 3)
+    same = stencil27_rows(n, 0, n ** 3, nz=n)
+    assert np.array_equal(cube.row_ptr, same.row_ptr)
+    assert np.array_equal(cube.col_idx, same.col_idx)
+    box = stencil27_rows(n, 0, 3 * n ** 3, nz=3 * n)
+    assert box.num_cols == 3 * n ** 3
+    # the first row of slab 1 (z = n) couples to z = n - 1 (slab 0) and z = n + 1
+    i = n ** 3 + n * n + n + 1  # interior in x, y; z = n + 1
+    c = box.col_idx[box.row_ptr[i]:box.row_ptr[i + 1]]
+    assert len(c) == 27 and c.min() == i - n * n - n - 1 and c.max() == i + n * n + n + 1
+    j = n ** 3 + n + 1  # z = n, slab edge
+    c = box.col_idx[box.row_ptr[j]:box.row_ptr[j + 1]]
+    assert len(c) == 27 and c.min() < n ** 3
