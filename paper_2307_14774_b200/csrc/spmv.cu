@@ -162,18 +162,40 @@ struct LaneMasks {
     }
 };
 
+// x gathers: read-only path; with SPC5_X_EVICT_LAST an L2 evict-last policy
+// (the per-load form of an L2 persistence window for x)
+#ifndef SPC5_X_EVICT_LAST
+#define SPC5_X_EVICT_LAST 0
+#endif
+__device__ __forceinline__ uint64_t x_policy() {
+    uint64_t pol;
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
+    return pol;
+}
 __device__ __forceinline__ double ldg_pred(const double *p, bool pred) {
     double v = 0.0;
+#if SPC5_X_EVICT_LAST
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n}"
+        : "+d"(v)
+        : "l"(p), "r"((int)pred), "l"(x_policy()));
+#else
     asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f64 %0, [%1];\n}"
         : "+d"(v)
         : "l"(p), "r"((int)pred));
+#endif
     return v;
 }
 __device__ __forceinline__ float ldg_pred(const float *p, bool pred) {
     float v = 0.0f;
+#if SPC5_X_EVICT_LAST
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.L2::cache_hint.f32 %0, [%1], %3;\n}"
+        : "+f"(v)
+        : "l"(p), "r"((int)pred), "l"(x_policy()));
+#else
     asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.f32 %0, [%1];\n}"
         : "+f"(v)
         : "l"(p), "r"((int)pred));
+#endif
     return v;
 }
 template <typename T>
