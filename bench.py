@@ -479,7 +479,7 @@ def main():
                          "strong = the config's one matrix split over the GPUs (config 5)")
     args = ap.parse_args()
     if args.scaling is None:
-        args.scaling = "weak" if args.config == 2 else "strong"
+        args.scaling = "weak" if args.config in (2, 6) else "strong"
     if args.warmup < 3:
         args.warmup = 3
     from paper_2307_14774_b200.workloads import CONFIGS

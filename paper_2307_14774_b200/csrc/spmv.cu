@@ -741,6 +741,8 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t 
         } else if constexpr (R == 8) {  // pair slots: steps of 6 / 12 / 18 blocks
             if (maxlen <= 6) {
                 lpp_steps2<T, MT, R, 6, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+            } else if (maxlen <= 9) {  // one step of block slots (beta(8,16) stencil rows)
+                lpp_steps2<T, MT, R, 9, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else if (maxlen <= 12) {
                 lpp_steps2<T, MT, R, 12, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else {
@@ -1094,7 +1096,11 @@ template <typename T, typename MT, int R, bool GENERIC>
 #ifndef SPC5_K2_MAXREG
 #define SPC5_K2_MAXREG 168
 #endif
-__global__ void __maxnreg__(SPC5_K2_MAXREG) spmv_kernel(const SpmvArgs a) {
+#ifndef SPC5_K2_MAXREG_F32
+#define SPC5_K2_MAXREG_F32 SPC5_K2_MAXREG
+#endif
+__global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG)
+    spmv_kernel(const SpmvArgs a) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;  // mask bytes per lane (<= 16)
     extern __shared__ __align__(128) uint8_t smem[];

@@ -205,4 +205,9 @@ CONFIGS = {
             cols=3 * FEM_NODES, formats=[(4, 8), (8, 8)]),
     5: dict(name="stencil27_400cubed", precision="f64", n=400,
             formats=[(1, 8), (2, 8), (4, 8), (8, 8)]),
+    # the fp32 halves of configs 2 and 5 (BASELINE config 5 names both precisions)
+    6: dict(name="stencil27_128cubed_f32", precision="f32", n=128,
+            formats=[(1, 16), (2, 16), (4, 16), (8, 16)]),
+    7: dict(name="stencil27_400cubed_f32", precision="f32", n=400,
+            formats=[(1, 16), (2, 16), (4, 16), (8, 16)]),
 }
