@@ -230,6 +230,35 @@ __device__ __forceinline__ void mac<float>(double &acc, float v, float xv) {
     acc += (double)__fmul_rn(v, xv);
 }
 
+// Slot-call partial sums: f64 products go straight into the f64 row sum; f32
+// products of one call (<= U*NS of them) are summed with f32 FMAs and the
+// partial is added to the f64 row sum once (SPC5_F32_PARTIAL; the error of a
+// partial is <= U*NS f32 roundings of its own sum of |products|, well inside
+// the reference's f32 budget nnz_row * eps * sum|p|, kernels.py:305-312).
+#ifndef SPC5_F32_PARTIAL
+#define SPC5_F32_PARTIAL 1
+#endif
+template <typename T>
+struct SlotSum {  // f64 matrices: the row sum itself
+    double &acc;
+    __device__ __forceinline__ explicit SlotSum(double &a) : acc(a) {}
+    __device__ __forceinline__ void add(double v, double x) { acc = fma(v, x, acc); }
+    __device__ __forceinline__ void done() {}
+};
+template <>
+struct SlotSum<float> {
+    double &acc;
+    float part = 0.0f;
+    __device__ __forceinline__ explicit SlotSum(double &a) : acc(a) {}
+    __device__ __forceinline__ void add(float v, float x) {
+        if (SPC5_F32_PARTIAL) part = __fmaf_rn(v, x, part);
+        else mac<float>(acc, v, x);
+    }
+    __device__ __forceinline__ void done() {
+        if (SPC5_F32_PARTIAL) acc += (double)part;
+    }
+};
+
 // highest set bit of a non-zero word (PTX bfind -> SASS FLO)
 __device__ __forceinline__ uint32_t bfind(uint32_t m) {
     uint32_t r;
@@ -317,14 +346,16 @@ __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h
             xv[k][u] = ldg_pred(x + (col[k] + pos), u < h0[k]);
         }
     }
+    SlotSum<T> sum(acc);
 #pragma unroll
     for (int k = 0; k < U; ++k) {
 #pragma unroll
         for (int u = 0; u < NS; ++u) {
             const T vv = lds_pred<T>(vtop[k] - (uint32_t)(u * sizeof(T)), u < h0[k]);
-            mac<T>(acc, vv, xv[k][u]);
+            sum.add(vv, xv[k][u]);
         }
     }
+    sum.done();
 }
 
 // One panel row of U blocks with a warp-uniform slot count: the smallest
@@ -378,6 +409,8 @@ __device__ __forceinline__ void row_slots_sep(double (&acc)[U], uint32_t (&m)[U]
             xv[k][u] = ldg_pred(x + (col[k] + pos), u < h0[k]);
         }
     }
+    // one product per block and slot here (~1 per block in balanced lane
+    // ranges): f32 partials per block measured slower than the f64 adds
 #pragma unroll
     for (int k = 0; k < U; ++k) {
 #pragma unroll
@@ -573,14 +606,16 @@ __device__ __forceinline__ void pair_slots(double &acc, const uint32_t (&m)[2 * 
             xv[i][u] = ldg_pred(x + xi, u < c[i]);
         }
     }
+    SlotSum<T> sum(acc);
 #pragma unroll
     for (int i = 0; i < UP; ++i) {
 #pragma unroll
         for (int u = 0; u < NS; ++u) {
             const uint32_t va = (u < hh[i] ? vhi[i] : vlo[i]) - (uint32_t)u * SZ;
-            mac<T>(acc, lds_pred<T>(va, u < c[i]), xv[i][u]);
+            sum.add(lds_pred<T>(va, u < c[i]), xv[i][u]);
         }
     }
+    sum.done();
 }
 
 __device__ __forceinline__ uint32_t lds_mask_row(uint32_t addr, int mb) {
