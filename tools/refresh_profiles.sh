@@ -22,9 +22,11 @@ for f in "1,8" "2,8" "4,8" "8,8"; do
 done
 python tools/summarize_profiles.py $R $O/launches.csv $reps > $O/summary.txt 2>&1
 cp profiles/launches_$R.csv profiles/ncu_$R.csv profiles/traffic.json $O/ 2>/dev/null
-for c in 3 4; do
+python -c "import __graft_entry__ as g; g.smoke()" > $O/smoke.log 2>&1
+for c in 1 3 4 6; do
   timeout 900 python bench.py --config $c --steps 50 --warmup 5 --no-e2e > $O/bench_c$c.json 2>&1
 done
+timeout 600 python bench.py --impl reference --steps 3 --warmup 3 > $O/bench_reference.json 2>&1
 timeout 1500 python bench.py --config 5 --steps 10 --warmup 3 --no-e2e --no-cpu-baseline \
   > $O/bench_c5.json 2>&1
 ls -la $O
