@@ -174,6 +174,9 @@ __device__ __forceinline__ uint64_t x_policy() {
 }
 __device__ __forceinline__ double ldg_pred(const double *p, bool pred) {
     double v = 0.0;
+#ifdef SPC5_X_PROBE_L1  // timing probe only (wrong results): gathers folded into a few 4 KB windows (L1 hits)
+    p = reinterpret_cast<const double *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)0x1fff000);
+#endif
 #if SPC5_X_EVICT_LAST
     asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.L2::cache_hint.f64 %0, [%1], %3;\n}"
         : "+d"(v)
@@ -187,6 +190,9 @@ __device__ __forceinline__ double ldg_pred(const double *p, bool pred) {
 }
 __device__ __forceinline__ float ldg_pred(const float *p, bool pred) {
     float v = 0.0f;
+#ifdef SPC5_X_PROBE_L1
+    p = reinterpret_cast<const float *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)0x1fff000);
+#endif
 #if SPC5_X_EVICT_LAST
     asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.global.nc.L2::cache_hint.f32 %0, [%1], %3;\n}"
         : "+f"(v)
