@@ -167,11 +167,13 @@ struct LaneMasks {
 #ifndef SPC5_X_EVICT_LAST
 #define SPC5_X_EVICT_LAST 0
 #endif
+#if SPC5_X_EVICT_LAST
 __device__ __forceinline__ uint64_t x_policy() {
     uint64_t pol;
     asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
     return pol;
 }
+#endif
 __device__ __forceinline__ double ldg_pred(const double *p, bool pred) {
     double v = 0.0;
 #ifdef SPC5_X_PROBE_L1  // timing probe only (wrong results): gathers folded into a few 4 KB windows (L1 hits)
@@ -527,57 +529,6 @@ __device__ __forceinline__ uint32_t row_rt(const LaneMasks<LB> &mk, int rr) {
 // matrices).  The plan's records give the first block and first value
 // (16 bits each, relative to the chunk) of every (panel, sub-range), so a
 // lane starts at once.
-// Lane's row over blocks s .. s+my-1 of its panel range, U blocks per step.
-template <typename T, typename MT, int R, int U>
-__device__ __forceinline__ void lpp_steps(double &acc, int maxlen, int my, int s, int rr,
-                                          uint32_t vaddr, uint32_t a_col, uint32_t a_mask,
-                                          uint32_t a_zero, const T *__restrict__ x) {
-    constexpr int MB = (int)sizeof(MT);
-    constexpr int LB = R * MB;
-    constexpr int N = LaneMasks<LB>::N;
-    constexpr uint32_t M = MB == 1 ? 0xffu : 0xffffu;
-    // this lane's row inside a block's packed masks, fixed for the chunk
-    const int bit = rr * 8 * MB;
-    uint32_t keep[N];  // bits of the rows below rr
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-        const int lo = i * 32;
-        keep[i] = bit >= lo + 32 ? 0xffffffffu : (bit <= lo ? 0u : ((1u << (bit - lo)) - 1u));
-    }
-    const int wsel = bit >> 5, sh = bit & 31;
-    for (int j = 0; j < maxlen; j += U) {
-        uint32_t col[U], vr[U], m[U];
-        int h[U], cm = 0;
-        uint32_t vnext = vaddr;
-#pragma unroll
-        for (int k = 0; k < U; ++k) {
-            const bool ok = j + k < my;
-            const uint32_t bk = (uint32_t)(ok ? s + j + k : 0);
-            col[k] = lds_u32(a_col + bk * 4u);
-            LaneMasks<LB> mk;
-            mk.load(ok ? a_mask + bk * LB : a_zero);  // past the range: 16 zero bytes
-            // block k's values: rows 0..R-1 in order; this lane's row starts
-            // after the rows below it
-            int below = 0, total = 0;
-#pragma unroll
-            for (int i = 0; i < N; ++i) {
-                total += __popc(mk.w[i]);
-                if (R > 1) below += __popc(mk.w[i] & keep[i]);
-            }
-            vr[k] = vnext + (uint32_t)below * (uint32_t)sizeof(T);
-            vnext += (uint32_t)total * (uint32_t)sizeof(T);
-            uint32_t w = mk.w[0];
-#pragma unroll
-            for (int i = 1; i < N; ++i) w = wsel == i ? mk.w[i] : w;
-            m[k] = R == 1 ? mk.w[0] : (w >> sh) & M;
-            h[k] = __popc(m[k]);
-            cm = max(cm, h[k]);
-        }
-        vaddr = vnext;
-        row_dispatch<T, U>(acc, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
-    }
-}
-
 // Pair slots (lane-per-panel-row steps): blocks 2i and 2i+1 of the lane's row
 // form one 2*BB-bit word, so a step costs max-over-lanes(bits of a PAIR)
 // slots instead of twice max-over-lanes(bits of a BLOCK) -- the row's bits
@@ -641,9 +592,6 @@ __device__ __forceinline__ uint32_t lds_mask_row(uint32_t addr, int mb) {
 // popcounts the other rows' masks.  Field widths: FB=8 (vs<=8: h<=8, sums
 // over 8 rows <= 64, prefix of 3 totals + rows below <= 248) or FB=16.
 // PAIRS (U even): steps whose pair slots beat block slots use pair_slots.
-#ifndef SPC5_LPP2
-#define SPC5_LPP2 1
-#endif
 template <typename T, typename MT, int R, int U, bool PAIRS>
 __device__ __forceinline__ void lpp_steps2(double &acc, int maxlen, int my, int s, int rr, int lg,
                                            int lane, uint32_t vaddr, uint32_t a_col,
@@ -743,12 +691,9 @@ __device__ __forceinline__ void lpp_steps2(double &acc, int maxlen, int my, int 
 
 template <typename T, typename MT, int R, bool GENERIC>
 __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int npc,
-                                          int lg, bool head_mid, uint32_t a_zero, uint32_t a_rec,
-                                          uint32_t a_col, uint32_t a_mask,
-                                          uint32_t a_val, int lane, const T *__restrict__ x,
-                                          T *__restrict__ y) {
-    constexpr int MB = (int)sizeof(MT);
-    constexpr int LB = R * MB;
+                                          int lg, bool head_mid, uint32_t a_rec, uint32_t a_col,
+                                          uint32_t a_mask, uint32_t a_val, int lane,
+                                          const T *__restrict__ x, T *__restrict__ y) {
     constexpr int LGR = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
     const int G = 1 << lg;
     const int sub = lane & (G - 1);
@@ -771,15 +716,7 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t 
         // U blocks per step (U from the longest lane range): all their x
         // gathers are in flight before the first FMA; values still accumulate
         // in storage order
-        if (!SPC5_LPP2) {
-            if (maxlen <= 3) {
-                lpp_steps<T, MT, R, 3>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
-            } else if (maxlen <= 6) {
-                lpp_steps<T, MT, R, 6>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
-            } else {
-                lpp_steps<T, MT, R, 9>(acc, maxlen, my, s, rr, vaddr, a_col, a_mask, a_zero, x);
-            }
-        } else if constexpr (R == 8) {  // pair slots: steps of 6 / 12 / 18 blocks
+        if constexpr (R == 8) {  // pair slots: steps of 6 / 12 / 18 blocks
             if (maxlen <= 6) {
                 lpp_steps2<T, MT, R, 6, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else if (maxlen <= 9) {  // one step of block slots (beta(8,16) stencil rows)
@@ -1220,7 +1157,7 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
 
         if (flags & 4) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
-                                         sbase + 48, a_rp, a_col, a_mask, a_val, lane, x, y);
+                                         a_rp, a_col, a_mask, a_val, lane, x, y);
         } else if (!slow && SPC5_BLR) {  // balanced lane ranges
             blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, sbase + 48, a_bits,
                                                            a_rp, a_col, a_mask, a_val, lane, x, y);
