@@ -127,6 +127,15 @@ __global__ void targets_kernel(int64_t num_panels, const int64_t *__restrict__ r
     cand[c] = rowptr[P];
 }
 
+// (a') panel-count targets: a chunk every ppc panels (regular matrices, so
+// every lane-per-panel-row step of the chunk is a full warp)
+__global__ void targets_panels_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
+                                      int64_t ppc, int64_t num_targets, int64_t *cand) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= num_targets) return;
+    cand[c] = rowptr[min(c * ppc, num_panels)];
+}
+
 // (b) forced splits inside giant panels at global multiples of kSplit
 __device__ __forceinline__ int64_t split_count(int64_t s, int64_t e, int64_t base,
                                                int64_t kSplit) {
@@ -562,10 +571,10 @@ int validate_structure(const Matrix &m, cudaStream_t st) {
 // GLOBAL multiples of kSplit (so a long panel is cut where its own position
 // says, independent of cb, shards and ranges).  Fills chunk_b/v/p (+sentinels),
 // the split-chunk list and the carry slots.
-static int build_chunks(Matrix &m, int64_t cb, cudaStream_t st) {
+static int build_chunks(Matrix &m, int64_t cb, int64_t ppc, cudaStream_t st) {
     Plan &P = m.plan;
     const int64_t nb = m.num_blocks, np = m.num_panels;
-    const int64_t num_targets = cdiv(nb, cb);
+    const int64_t num_targets = ppc ? cdiv(np, ppc) : cdiv(nb, cb);
     int64_t *split_counts = nullptr;
     SPC5_TRY(dev_alloc(&split_counts, (size_t)np));
     split_count_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
@@ -581,8 +590,12 @@ static int build_chunks(Matrix &m, int64_t cb, cudaStream_t st) {
     int64_t *cand = nullptr, *sorted = nullptr;
     SPC5_TRY(dev_alloc(&cand, (size_t)ncand));
     SPC5_TRY(dev_alloc(&sorted, (size_t)ncand + 1));
-    targets_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(np, m.rowptr, cb,
-                                                                      num_targets, cand);
+    if (ppc)
+        targets_panels_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(
+            np, m.rowptr, ppc, num_targets, cand);
+    else
+        targets_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(np, m.rowptr, cb,
+                                                                          num_targets, cand);
     if (num_forced)
         split_fill_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
                                                                     P.split_len, split_incl,
@@ -745,8 +758,25 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     // GPU (SMs x 12) gets about one, so a product is one chunk deep
     int64_t cb_max = 512;
     while (cb_max > 32 && nb / cb_max < (int64_t)m.sm_count * 12) cb_max >>= 1;
-    for (int64_t cb = cb_max;; cb >>= 1) {
-        SPC5_TRY(build_chunks(m, cb, st));
+    // Chunk targets, largest first.  Regular matrices: k warp steps of panels
+    // per chunk (k * 32/r panels, the whole chunk in full lane-per-panel-row
+    // steps, no partly empty last step); accepted while no chunk exceeds the
+    // average by 25 %.  Then block-count targets, powers of two.
+    struct Target {
+        int64_t cb, ppc;
+    };
+    std::vector<Target> targets;
+    {
+        const double avg = (double)nb / (double)std::max<int64_t>(np, 1);
+        const int64_t lanes = 32 / m.r;
+        if (!getenv("SPC5_CB_POW2") && avg > 0.0)
+            for (int64_t k = (int64_t)((double)cb_max / ((double)lanes * avg)); k >= 1; --k)
+                targets.push_back({(int64_t)((double)(k * lanes) * avg), k * lanes});
+        for (int64_t cb = cb_max; cb >= 1; cb >>= 1) targets.push_back({cb, 0});
+    }
+    for (size_t ti = 0;; ++ti) {
+        const int64_t cb = targets[ti].cb, ppc = targets[ti].ppc;
+        SPC5_TRY(build_chunks(m, cb, ppc, st));
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
@@ -782,8 +812,9 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.lay_val = P.lay_mask + a16(mb * lb + std::max<int64_t>(32, ((m.r == 8 ? 18 : 9) - 1) * lb));
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
                              128 * 128);
-        if (P.slot_bytes <= slot_cap || cb == 1) break;
-        if (cb <= 32 && P.slot_bytes <= 14 * 1024) break;
+        const bool regular = !ppc || P.max_chunk_blocks * 4 <= cb * 5;
+        if (regular && (P.slot_bytes <= slot_cap || cb == 1 || ti + 1 >= targets.size())) break;
+        if (regular && cb <= 32 && P.slot_bytes <= 14 * 1024) break;
         free_chunks(P);
         dev_free(P.chunk_flags);
         P.chunk_flags = nullptr;

@@ -1244,6 +1244,16 @@ int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
         if (it == cache.end()) {
             SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                            227 * 1024));
+            // SPC5_CARVEOUT: ask for no more shared memory than the ring of the
+            // resident CTAs needs, so the rest stays L1 for the x gathers
+            if (getenv("SPC5_CARVEOUT")) {
+                int ps = 0;
+                SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kernel, wpc * 32, smem));
+                const int pct = (int)std::min<size_t>(
+                    100, (std::max(ps, 1) * (smem + 1024) * 100 + 228 * 1024 - 1) / (228 * 1024));
+                SPC5_CUDA(cudaFuncSetAttribute(kernel,
+                                               cudaFuncAttributePreferredSharedMemoryCarveout, pct));
+            }
             SPC5_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, wpc * 32,
                                                                     smem));
             it = cache.emplace(key, std::max(per_sm, 1)).first;
