@@ -772,8 +772,19 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         if (!getenv("SPC5_CB_POW2") && avg > 0.0)
             for (int64_t k = (int64_t)((double)cb_max / ((double)lanes * avg)); k >= 1; --k)
                 targets.push_back({(int64_t)((double)(k * lanes) * avg), k * lanes});
-        for (int64_t cb = cb_max; cb >= 1; cb >>= 1) targets.push_back({cb, 0});
+        // block-count targets: powers of two; for r = 1 also their 3/4 (config
+        // 3 beta(1,16): 384-block chunks 392 us, 512: 483 us; for r > 1 the
+        // 3/4 steps measured slower)
+        for (int64_t cb = cb_max; cb >= 1; cb >>= 1) {
+            targets.push_back({cb, 0});
+            if (m.r == 1 && !getenv("SPC5_CB_POW2") && cb >= 8) targets.push_back({cb * 3 / 4, 0});
+        }
+        if (const char *e = getenv("SPC5_CB")) targets = {{std::max(1, atoi(e)), 0}};  // tuning
     }
+    if (const char *e = getenv("SPC5_SLOT_B")) slot_cap = std::max(1024, atoi(e));
+    // irregular r = 1 matrices (block-count targets): slots <= 8 KB
+    int64_t irr_cap = m.r == 1 ? std::min<int64_t>(slot_cap, 8192) : slot_cap;
+    if (const char *e = getenv("SPC5_SLOT_B_IRR")) irr_cap = std::max(1024, atoi(e));
     for (size_t ti = 0;; ++ti) {
         const int64_t cb = targets[ti].cb, ppc = targets[ti].ppc;
         SPC5_TRY(build_chunks(m, cb, ppc, st));
@@ -813,7 +824,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
                              128 * 128);
         const bool regular = !ppc || P.max_chunk_blocks * 4 <= cb * 5;
-        if (regular && (P.slot_bytes <= slot_cap || cb == 1 || ti + 1 >= targets.size())) break;
+        const int64_t cap = ppc ? slot_cap : irr_cap;
+        if (regular && (P.slot_bytes <= cap || cb == 1 || ti + 1 >= targets.size())) break;
         if (regular && cb <= 32 && P.slot_bytes <= 14 * 1024) break;
         free_chunks(P);
         dev_free(P.chunk_flags);
