@@ -428,17 +428,20 @@ __device__ __forceinline__ void row_slots_sep(double (&acc)[U], uint32_t (&m)[U]
         }
     }
 }
-template <typename T, int U>
+// OPQ: opaque slot-count compares (if-chains) or plain ones (the compiler's
+// jump table); measured per format, the jump table is faster only in the
+// r = 2 kernels (config 3 beta(2,16): 659 vs 752 us)
+template <typename T, int U, bool OPQ = true>
 __device__ __forceinline__ void row_dispatch_sep(double (&acc)[U], uint32_t (&m)[U], int (&h)[U],
                                                  const T *__restrict__ x,
                                                  const uint32_t (&col)[U],
                                                  const uint32_t (&vaddr)[U], int cmax) {
     if (cmax <= 0) return;
-    if (ueq(cmax, 1)) {
+    if ((OPQ ? ueq(cmax, 1) : cmax == 1)) {
         row_slots_sep<T, U, 1>(acc, m, h, x, col, vaddr);
-    } else if (ueq(cmax, 2)) {
+    } else if ((OPQ ? ueq(cmax, 2) : cmax == 2)) {
         row_slots_sep<T, U, 2>(acc, m, h, x, col, vaddr);
-    } else if (ueq(cmax, 3)) {
+    } else if ((OPQ ? ueq(cmax, 3) : cmax == 3)) {
         row_slots_sep<T, U, 3>(acc, m, h, x, col, vaddr);
     } else {
         for (int done = 0; done < cmax; done += 4) row_slots_sep<T, U, 4>(acc, m, h, x, col, vaddr);
@@ -834,7 +837,7 @@ __device__ __forceinline__ void lpb_chunk(const SpmvArgs &a, int64_t c, int64_t 
                 vb[k] += (uint32_t)__popc(mrow) * (uint32_t)sizeof(T);
                 acc[g][k] = 0.0;
             }
-            row_dispatch_sep<T, K>(acc[g], m, h, x, colk, vr, __reduce_max_sync(kFull, cm));
+            row_dispatch_sep<T, K, R != 2>(acc[g], m, h, x, colk, vr, __reduce_max_sync(kFull, cm));
         }
         // ---- reduce the windows in order
 #pragma unroll
@@ -984,7 +987,7 @@ __device__ __forceinline__ void blr_chunk(const SpmvArgs &a, int64_t c, int64_t 
                 vbk[k] += (uint32_t)h[k] * (uint32_t)sizeof(T);
                 pg[k] = 0.0;
             }
-            row_dispatch_sep<T, U>(pg, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
+            row_dispatch_sep<T, U, R != 2>(pg, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
 #pragma unroll
             for (int k = 0; k < U; ++k) part[k][g] = pg[k];
         }
