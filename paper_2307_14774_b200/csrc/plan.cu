@@ -769,9 +769,12 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     {
         const double avg = (double)nb / (double)std::max<int64_t>(np, 1);
         const int64_t lanes = 32 / m.r;
-        if (!getenv("SPC5_CB_POW2") && avg > 0.0)
-            for (int64_t k = (int64_t)((double)cb_max / ((double)lanes * avg)); k >= 1; --k)
+        // (at least one block per panel on average; at most 8 candidates)
+        if (!getenv("SPC5_CB_POW2") && avg >= 1.0) {
+            const int64_t kmax = (int64_t)((double)cb_max / ((double)lanes * avg));
+            for (int64_t k = kmax; k >= 1 && k > kmax - 8; --k)
                 targets.push_back({(int64_t)((double)(k * lanes) * avg), k * lanes});
+        }
         // block-count targets: powers of two; for r = 1 also their 3/4 (config
         // 3 beta(1,16): 384-block chunks 392 us, 512: 483 us; for r > 1 the
         // 3/4 steps measured slower)
