@@ -769,11 +769,22 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     {
         const double avg = (double)nb / (double)std::max<int64_t>(np, 1);
         const int64_t lanes = 32 / m.r;
-        // (at least one block per panel on average; at most 8 candidates)
+        // (at least one block per panel on average; candidates whose average
+        // slot bytes already exceed the cap are not built)
+        const double per_blk = 4.0 + (double)m.r * m.mask_bytes() +
+                               (double)m.value_bytes() * (double)m.nnz / (double)std::max<int64_t>(nb, 1);
         if (!getenv("SPC5_CB_POW2") && avg >= 1.0) {
-            const int64_t kmax = (int64_t)((double)cb_max / ((double)lanes * avg));
-            for (int64_t k = kmax; k >= 1 && k > kmax - 8; --k)
+            int64_t kmax = (int64_t)((double)cb_max / ((double)lanes * avg));
+            while (kmax > 1 && (double)(kmax * lanes) * avg * per_blk > (double)slot_cap) --kmax;
+            for (int64_t k = kmax; k >= 1; --k) {
                 targets.push_back({(int64_t)((double)(k * lanes) * avg), k * lanes});
+                // k-1 full steps and a 7/8-full last one, when k full ones
+                // just miss the slot (fp32 beta(2,16): 30 panels, not 16)
+                if (k > 1 && lanes >= 8) {
+                    const int64_t ppc = k * lanes - lanes / 8;
+                    targets.push_back({(int64_t)((double)ppc * avg), ppc});
+                }
+            }
         }
         // block-count targets: powers of two; for r = 1 also their 3/4 (config
         // 3 beta(1,16): 384-block chunks 392 us, 512: 483 us; for r > 1 the
