@@ -4,11 +4,12 @@ Drop-in for the hot path of the reference package ``spc5``
 (/root/reference/pkg/src/spc5/__init__.py:11-21 names): CSR->SPC5 conversion,
 the SpMV entry points, the nnz-balanced partition and the timing harness,
 backed by hand-written sm_100a CUDA kernels in ``libspc5_b200.so`` (C ABI:
-include/spc5_b200.h).  Importing this package loads the library; there is no
-CPU fallback.
+include/spc5_b200.h).  The library is loaded on the first device call
+(``_native.load()``) and a missing library raises ImportError there; there is
+no CPU fallback.
 """
 
-from . import _native  # noqa: F401  (loads libspc5_b200.so, raises ImportError if absent)
+from . import _native  # noqa: F401  (loads libspc5_b200.so on first use)
 from .blocks import (VALID_R, VALID_VS, FillingStats, Spc5Matrix, csr_to_spc5,
                      csr_to_spc5_device, filling_stats, footprint_comparison, load_spc5,
                      mask_dtype, save_spc5, spc5_to_csr, validate_spc5)

@@ -1,13 +1,18 @@
 """ctypes binding of libspc5_b200.so (the C ABI declared in include/spc5_b200.h).
 
-Loaded eagerly at package import; a missing or unloadable library is an
-ImportError -- there is no CPU fallback anywhere in this package.
+Loaded on first use of ``lib`` (any entry point of the package that touches
+the device); a missing or unloadable library raises ImportError there --
+there is no CPU fallback anywhere in this package.  Loading lazily keeps the
+host-only helpers (the seeded workload generators, the CSV records) usable
+without the CUDA library, e.g. by bench.py's reference arm, which must not
+load it.
 """
 
 from __future__ import annotations
 
 import ctypes
 import os
+import threading
 from pathlib import Path
 
 LIB_PATH = Path(__file__).resolve().parent / "libspc5_b200.so"
@@ -83,7 +88,24 @@ def _load():
     return lib
 
 
-lib = _load()
+_lib = None
+_lib_lock = threading.Lock()
+
+
+def load():
+    """The loaded library (loads it on the first call)."""
+    global _lib
+    if _lib is None:
+        with _lib_lock:
+            if _lib is None:
+                _lib = _load()
+    return _lib
+
+
+def __getattr__(name):  # PEP 562: ``nat.lib`` loads on first access
+    if name == "lib":
+        return load()
+    raise AttributeError(name)
 
 
 class Spc5Error(RuntimeError):
@@ -94,7 +116,7 @@ def check(status: int) -> None:
     """Map a C status to the exception the reference raises."""
     if status == OK:
         return
-    msg = lib.spc5_last_error().decode("utf-8", "replace")
+    msg = load().spc5_last_error().decode("utf-8", "replace")
     if status == EINVAL:
         raise ValueError(msg)
     if status == ECURSOR:
@@ -105,10 +127,10 @@ def check(status: int) -> None:
 
 
 def last_launch_count() -> int:
-    return int(lib.spc5_last_launch_count())
+    return int(load().spc5_last_launch_count())
 
 
 def device_count() -> int:
     n = ctypes.c_int(0)
-    lib.spc5_device_count(ctypes.byref(n))
+    load().spc5_device_count(ctypes.byref(n))
     return int(n.value)

@@ -14,7 +14,8 @@ NVLink/NVSwitch):
   panel-local), and ``block_base`` keeps the warp windows on the global grid.
 * iterated products (BASELINE config 5): the local K2 writes its y-slice
   straight into the next x buffer, then an all-gather of the unequal slices
-  (one broadcast per owner rank, batched) fills the rest and the buffers swap.
+  (one NCCL group of point-to-point sends/receives) fills the rest and the
+  buffers swap.
 
 The local product is a callable so the host logic is testable on CPU with the
 gloo backend (tests/test_distributed.py); on GPUs it is the C-ABI SpMV.
@@ -85,25 +86,46 @@ def shard_layout(row_ptr, r: int, workers: int) -> ShardLayout:
     return ShardLayout(r, len(row_ptr) - 1, panel_partition(row_ptr, r, workers))
 
 
-def allgather_slices(x, layout: ShardLayout, rank: int, world: int) -> None:
+def allgather_slices(x, layout: ShardLayout, rank: int, world: int, mode: str = "p2p") -> None:
     """Fill every rank's copy of x with the owners' slices (allgatherv in place).
 
-    The slices are unequal (nnz-balanced), so each owner broadcasts its slice
-    into the same view on every rank; the P broadcasts are issued together and
-    waited on once (NCCL runs them as one batch of collectives).
+    The slices are unequal (nnz-balanced row-panel shards), so this is an
+    all-gather-v.  mode "p2p" (default): one batch of point-to-point
+    operations -- this rank's slice sent to every peer, every peer's slice
+    received into its place in x -- issued as ONE NCCL group
+    (``batch_isend_irecv`` -> ncclGroupStart/End), so every transfer is in
+    flight at once over NVSwitch.  mode "bcast": one broadcast per owner,
+    coalesced (the A/B alternative).  No staging copies either way.
     """
     import torch.distributed as dist
-    reqs = []
+    if world == 1:
+        return
+    mine = layout.rows(rank)
+    if mode == "bcast":
+        reqs = []
+        for k in range(world):
+            lo, hi = layout.rows(k)
+            if hi > lo:
+                reqs.append(dist.broadcast(x[lo:hi], src=k, async_op=True))
+        for q in reqs:
+            q.wait()
+        return
+    ops = []
     for k in range(world):
+        if k == rank:
+            continue
         lo, hi = layout.rows(k)
+        if mine[1] > mine[0]:
+            ops.append(dist.P2POp(dist.isend, x[mine[0]:mine[1]], k))
         if hi > lo:
-            reqs.append(dist.broadcast(x[lo:hi], src=k, async_op=True))
-    for q in reqs:
-        q.wait()
+            ops.append(dist.P2POp(dist.irecv, x[lo:hi], k))
+    if ops:
+        for q in dist.batch_isend_irecv(ops):
+            q.wait()
 
 
 def iterate_products(x0, steps: int, layout: ShardLayout, rank: int, world: int,
-                     local_spmv: Callable, scale: float = 1.0):
+                     local_spmv: Callable, scale: float = 1.0, mode: str = "p2p"):
     """x_{t+1} = scale * A x_t for `steps` products, A split by row panels.
 
     local_spmv(x_full, y_out) computes this rank's rows of A.x into y_out
@@ -117,7 +139,7 @@ def iterate_products(x0, steps: int, layout: ShardLayout, rank: int, world: int,
         local_spmv(xa, xb[lo:hi])
         if scale != 1.0:
             xb[lo:hi] *= scale
-        allgather_slices(xb, layout, rank, world)
+        allgather_slices(xb, layout, rank, world, mode)
         xa, xb = xb, xa
     return xa
 
@@ -172,71 +194,54 @@ def iterate_products_fused(x0, steps: int, layout: ShardLayout, rank: int, world
     return ex.run(handle, x0, steps, scale).clone()
 
 
-# ----------------------------------------------------------------------------- bench
-def _shard_csr(cfg, lo, hi, prec):
-    """Device CSR of rows [lo, hi) of a BASELINE config (stencil / power-law / FEM)."""
-    import torch
 
-    from . import _native as nat
-    from .workloads import PL_N, PL_TABLE_BITS, powerlaw_len_table
-    tdt = torch.float64 if prec == "f64" else torch.float32
-    pc = 1 if prec == "f64" else 0
-    rows = hi - lo
-    rp = torch.empty(rows + 1, dtype=torch.int64, device="cuda")
-    gen = cfg.get("gen", "stencil")
-    table = torch.from_numpy(powerlaw_len_table()).to("cuda") if gen == "powerlaw" else None
-    nz = cfg.get("nz", cfg.get("n"))  # stencil box depth (weak scaling: n * ranks)
-    if gen == "stencil":
-        nat.check(nat.lib.spc5_gen_stencil27_box_rowptr(cfg["n"], nz, lo, hi, rp.data_ptr(), 0))
-    elif gen == "powerlaw":
-        nat.check(nat.lib.spc5_gen_powerlaw_rowptr(PL_N, lo, hi, 0, table.data_ptr(),
-                                                   PL_TABLE_BITS, rp.data_ptr(), 0))
-    else:
-        nat.check(nat.lib.spc5_gen_fem_rowptr(cfg["rows"] // 3, lo, hi, rp.data_ptr(), 0))
-    nnz = int(rp[-1])
-    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
-    va = torch.empty(max(nnz, 1), dtype=tdt, device="cuda")
-    if gen == "stencil":
-        nat.check(nat.lib.spc5_gen_stencil27_box_fill(cfg["n"], nz, lo, hi, pc, 0, 27.0,
-                                                      rp.data_ptr(), ci.data_ptr(),
-                                                      va.data_ptr(), 0))
-    elif gen == "powerlaw":
-        nat.check(nat.lib.spc5_gen_powerlaw_fill(PL_N, lo, hi, pc, 0, table.data_ptr(),
-                                                 PL_TABLE_BITS, rp.data_ptr(), ci.data_ptr(),
-                                                 va.data_ptr(), 0))
-    else:
-        nat.check(nat.lib.spc5_gen_fem_fill(cfg["rows"] // 3, lo, hi, pc, 0, rp.data_ptr(),
-                                            ci.data_ptr(), va.data_ptr(), 0))
+
+# ----------------------------------------------------------------------------- bench
+def _timed(fn, stream):
+    """Device time of fn() on `stream` (CUDA events), max over ranks."""
+    import torch
+    import torch.distributed as dist
     torch.cuda.synchronize()
-    return rp, ci, va
+    dist.barrier()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(stream)
+    out = fn()
+    e1.record(stream)
+    torch.cuda.synchronize()
+    t = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t), out
 
 
 def bench_distributed(args, formats) -> None:
     """bench.py for N > 1 (one process per GPU, torchrun, NCCL).
 
-    --scaling weak (the default for config 2): the matrix is the 27-point
-    stencil on an n x n x (n * N) box, so every rank owns one n^3 cube of rows
-    (its z-slab) -- the 1-GPU line's work per GPU.  --scaling strong (the
-    default for config 5, BASELINE's multi-GPU config, and the only form for
-    configs 3/4) splits the config's one matrix.  Either way the row panels are split nnz-balanced
-    over the ranks (panel_partition == partition_by_nnz) and every rank
-    converts only its rows.  One step = one product per format with x
+    --scaling strong (the default): the config's one matrix (BASELINE config
+    5: the 400^3 stencil) is split into nnz-balanced row-panel shards
+    (panel_partition == partition_by_nnz, computed from the generator's row
+    pointers alone) and every rank generates and converts only its rows.
+    --scaling weak: the 27-point stencil on an n x n x (n * N) box, one n^3
+    cube of rows per GPU.  One step = one product per format with x
     replicated and each rank writing its own y-slice: no data-path
-    collective.  The iterated form (x <- A.x refreshed by the NCCL all-gather
-    of the y-slices, BASELINE config 5) is timed after it and reported under
-    "iterated".  Times are device times (CUDA events), the max over ranks."""
+    collective (the bench `value`).  The iterated form -- x <- A.x/64 for
+    --iters products (BASELINE: 100), x refreshed between products by the
+    all-gather-v of the y-slices in one NCCL group -- is timed after it, A/B
+    against coalesced broadcasts and against the exchange fused into K2
+    (FusedExchange).  Times are device times (CUDA events), the max over
+    ranks."""
     import json
     import os
     import time
 
-    import numpy as np
+    os.environ.setdefault("NCCL_DEBUG", "INFO")
+    os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
     import torch
     import torch.distributed as dist
 
     from . import _native as nat
     from .blocks import csr_to_spc5_device, filling_stats, torch_stream
     from .kernels import spmv
-    from .workloads import CONFIGS, x_vector
+    from .workloads import CONFIGS, config_shape, device_rowptr, device_rows, x_vector
 
     rank = int(os.environ.get("RANK", "0"))
     world = int(os.environ.get("WORLD_SIZE", str(args.gpus)))
@@ -246,29 +251,26 @@ def bench_distributed(args, formats) -> None:
     cfg = CONFIGS[args.config]
     if cfg.get("gen") is None and "n" not in cfg:
         raise SystemExit(f"config {args.config}: no device generator for the multi-GPU bench")
-    weak = "n" in cfg and getattr(args, "scaling", "weak") == "weak"
+    weak = "n" in cfg and args.scaling == "weak"
     if weak:
         cfg = dict(cfg, nz=cfg["n"] * world)
     prec = cfg["precision"]
     tdt = torch.float64 if prec == "f64" else torch.float32
     vb = 8 if prec == "f64" else 4
-    N = cfg["n"] ** 2 * cfg["nz"] if weak else cfg["rows"]
-    C = N if "n" in cfg else cfg["cols"]
-    # global row pointers (structure only) for the partition
-    rp_all, ci_all, va_all = _shard_csr(cfg, 0, N, prec)
-    del ci_all, va_all
-    torch.cuda.empty_cache()
+    N, C = config_shape(cfg)
+    rp_all = device_rowptr(cfg, 0, N)  # structure only: the partition needs nothing else
     x_np = x_vector(C, prec)
     x0 = torch.from_numpy(x_np).to("cuda")
     st = torch_stream()
     stream = torch.cuda.current_stream()
     results, launches = {}, 0
-    from bench import ClockSampler, peaks  # noqa: E402  (repo root on sys.path)
+    from bench import ClockSampler, config_dict, peaks  # noqa: E402  (repo root on sys.path)
     sampler = ClockSampler(local) if rank == 0 else None
+    iters = max(1, args.iters)
     for (r, vs) in formats:
         layout = shard_layout(rp_all, r, world)
         lo, hi = layout.rows(rank)
-        rp, ci, va = _shard_csr(cfg, lo, hi, prec)
+        rp, ci, va = device_rows(cfg, lo, hi)
         s = csr_to_spc5_device(hi - lo, C, rp, ci, va, r, vs)
         del rp, ci, va
         torch.cuda.empty_cache()
@@ -279,61 +281,39 @@ def bench_distributed(args, formats) -> None:
         dist.all_reduce(counts)
         nnz_all, bytes_all = int(counts[0]), int(counts[1]) + vb * C * world
 
-        def product():
-            nat.check(nat.lib.spc5_spmv(h.ptr, x0.data_ptr(), y.data_ptr(), 0, st))
-            return nat.last_launch_count()
+        def products(n):
+            c = 0
+            for _ in range(n):
+                nat.check(nat.lib.spc5_spmv(h.ptr, x0.data_ptr(), y.data_ptr(), 0, st))
+                c += nat.last_launch_count()
+            return c
 
-        for _ in range(args.warmup):
-            product()
-        torch.cuda.synchronize()
-        dist.barrier()
+        products(args.warmup)
         if sampler is not None and not results:
             sampler.start()
             time.sleep(0.3)
-        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        e0.record(stream)
-        for _ in range(args.steps):
-            launches += product()
-        e1.record(stream)
-        torch.cuda.synchronize()
-        el = torch.tensor([e0.elapsed_time(e1) * 1e-3], device="cuda")
-        dist.all_reduce(el, op=dist.ReduceOp.MAX)
-        dist.barrier()
+        el, n_l = _timed(lambda: products(args.steps), stream)
+        launches += n_l
 
-        # iterated products: local K2 into the next x buffer + all-gather of the slices
+        # iterated products: local K2 into the next x buffer + all-gather-v of the slices
         def local_spmv(xf, yout, h=h):
             nat.check(nat.lib.spc5_spmv(h.ptr, xf.data_ptr(), yout.data_ptr(), 0, st))
 
-        iters = max(3, min(args.steps, 20))
         iterate_products(x0, 2, layout, rank, world, local_spmv, 1.0 / 64.0)
-        torch.cuda.synchronize()
-        dist.barrier()
-        i0, i1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        i0.record(stream)
-        iterate_products(x0, iters, layout, rank, world, local_spmv, 1.0 / 64.0)
-        i1.record(stream)
-        torch.cuda.synchronize()
-        it = torch.tensor([i0.elapsed_time(i1) * 1e-3], device="cuda")
-        dist.all_reduce(it, op=dist.ReduceOp.MAX)
+        it, xr = _timed(lambda: iterate_products(x0, iters, layout, rank, world, local_spmv,
+                                                 1.0 / 64.0), stream)
+        itb, xb = _timed(lambda: iterate_products(x0, iters, layout, rank, world, local_spmv,
+                                                  1.0 / 64.0, mode="bcast"), stream)
+        same_b = bool(torch.equal(xr, xb))
         # the same iterations with the exchange fused into K2 (NVLink stores)
-        fused = None
         try:
             ex = FusedExchange(C, tdt, layout, rank)
-            xf = ex.run(h, x0, iters, 1.0 / 64.0).clone()
-            xr = iterate_products(x0, iters, layout, rank, world, local_spmv, 1.0 / 64.0)
-            agree = bool(torch.equal(xf, xr))
-            torch.cuda.synchronize()
-            dist.barrier()
-            f0, f1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-            f0.record(stream)
-            ex.run(h, x0, iters, 1.0 / 64.0)
-            f1.record(stream)
-            torch.cuda.synchronize()
-            ft = torch.tensor([f0.elapsed_time(f1) * 1e-3], device="cuda")
-            dist.all_reduce(ft, op=dist.ReduceOp.MAX)
-            fused = {"seconds": float(ft), "bitwise_equal_to_allgather": agree}
+            ex.run(h, x0, 2, 1.0 / 64.0)
+            ft, xf = _timed(lambda: ex.run(h, x0, iters, 1.0 / 64.0).clone(), stream)
+            fused = {"seconds": ft, "bitwise_equal_to_allgather": bool(torch.equal(xf, xr))}
         except Exception as e:  # symmetric memory unavailable: report, keep the line
             fused = {"error": f"{type(e).__name__}: {e}"[:200]}
+        del xr, xb
 
         # end to end through the public API on pinned host buffers
         xp = torch.empty(C, dtype=tdt, pin_memory=True)
@@ -347,12 +327,12 @@ def bench_distributed(args, formats) -> None:
             spmv(s, xp.numpy(), yp.numpy()[:hi - lo])
         te = torch.tensor([time.perf_counter() - t0], device="cuda")
         dist.all_reduce(te, op=dist.ReduceOp.MAX)
-        results[f"b({r},{vs})"] = {"seconds": float(el), "nnz": nnz_all, "bytes": bytes_all,
-                                   "iter_seconds": float(it), "iters": iters,
+        results[f"b({r},{vs})"] = {"seconds": el, "nnz": nnz_all, "bytes": bytes_all,
+                                   "iter_seconds": it, "iter_bcast_seconds": itb,
+                                   "bcast_bitwise_equal": same_b, "iters": iters,
                                    "e2e_seconds": float(te), "e2e_steps": e2e_steps,
-                                   "fused": fused,
-                                   "h2d": vb * C, "d2h": vb * (hi - lo)}
-        del s, h, y
+                                   "fused": fused, "h2d": vb * C, "d2h": vb * (hi - lo)}
+        del s, h, y, xp, yp
         torch.cuda.empty_cache()
     clocks = sampler.stop() if sampler is not None else None
     h2d = torch.tensor([sum(v["h2d"] for v in results.values())], device="cuda")
@@ -367,21 +347,20 @@ def bench_distributed(args, formats) -> None:
         tot_t = sum(v["seconds"] for v in results.values())
         tot_b = sum(v["bytes"] for v in results.values()) * args.steps
         achieved = tot_b / tot_t / 1e9
+        conf = config_dict(args.config, formats, world, "weak" if weak else "strong")
+        if weak:
+            conf["workload"] = (f"stencil27_{cfg['n']}x{cfg['n']}x{cfg['nz']}_{prec} "
+                                f"({cfg['n']}^3 rows per GPU)")
+            conf["num_rows"] = conf["num_cols"] = N
         line = {"metric": "SpMV GFLOP/s (2*nnz/t)", "value": flops * args.steps / tot_t / 1e9,
                 "unit": "GFLOP/s", "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": tot_t / args.steps * 1e3,
                 "higher_is_better": True, "scaling": "weak" if weak else "strong",
-                "vs_baseline": None,
-                "dtype": prec, "data": "synthetic",
-                "config": {"workload": (f"stencil27_{cfg['n']}x{cfg['n']}x{cfg['nz']}_{prec}"
-                                        f" ({cfg['n']}^3 rows per GPU)" if weak else cfg["name"]),
-                           "formats": list(results),
-                           "num_rows": N, "nnz": results[next(iter(results))]["nnz"],
-                           "step": "y_f = A_f.x for every format; x replicated, each rank "
-                                   "writes its nnz-balanced row-panel slice of y",
-                           "order": "the K products of each format run back to back",
-                           "l2": "inputs larger than L2 (no flush)",
-                           "parallelism": f"row-panel shards x{world} (partition_by_nnz)"},
+                "vs_baseline": None, "dtype": prec, "data": "synthetic",
+                "config": conf,
+                "matrix": {"nnz": results[next(iter(results))]["nnz"],
+                           "step": "x replicated, each rank writes its nnz-balanced "
+                                   "row-panel slice of y"},
                 "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak * world,
                              "unit": "GB/s", "frac": achieved / (peak * world),
                              "traffic": None,
@@ -392,15 +371,18 @@ def bench_distributed(args, formats) -> None:
                                 "iterated_gflops": 2.0 * v["nnz"] * v["iters"]
                                 / v["iter_seconds"] / 1e9,
                                 "iterated_us": v["iter_seconds"] / v["iters"] * 1e6,
+                                "iterated_bcast_us": v["iter_bcast_seconds"] / v["iters"] * 1e6,
+                                "bcast_bitwise_equal": v["bcast_bitwise_equal"],
                                 "iterated_fused_us": (v["fused"]["seconds"] / v["iters"] * 1e6
                                                       if "seconds" in v["fused"] else None),
                                 "fused": v["fused"]}
                             for k, v in results.items()},
-                "iterated": {"step": "x <- A.x/64: local K2 into the next x + NCCL all-gather "
-                                     "of the y-slices (BASELINE config 5 form)",
-                             "value": flops * sum(v["iters"] for v in results.values())
-                             / len(results) / sum(v["iter_seconds"] for v in results.values())
-                             / 1e9, "unit": "GFLOP/s"},
+                "iterated": {"step": "x <- A.x/64: local K2 into the next x + all-gather-v of "
+                                     "the y-slices in one NCCL group (BASELINE config 5 form)",
+                             "iters_per_format": iters,
+                             "value": sum(2.0 * v["nnz"] * v["iters"] for v in results.values())
+                             / sum(v["iter_seconds"] for v in results.values()) / 1e9,
+                             "unit": "GFLOP/s"},
                 "gpu_launches": int(lc),
                 "clocks": clocks,
                 "e2e": {"value": sum(2.0 * v["nnz"] * v["e2e_steps"] for v in results.values())

@@ -211,3 +211,82 @@ CONFIGS = {
     7: dict(name="stencil27_400cubed_f32", precision="f32", n=400,
             formats=[(1, 16), (2, 16), (4, 16), (8, 16)]),
 }
+
+
+# ---------------------------------------------------------------- device twins
+def _gen_args(cfg):
+    gen = cfg.get("gen", "stencil")
+    nz = cfg.get("nz", cfg.get("n"))  # stencil box depth (weak scaling: n * ranks)
+    return gen, nz
+
+
+def device_rowptr(cfg, lo: int, hi: int):
+    """Row pointers (int64[hi-lo+1], device) of rows [lo, hi) of a config's
+    matrix, from the device generator alone -- no columns or values (the
+    partition needs only these)."""
+    import torch
+
+    from . import _native as nat
+    gen, nz = _gen_args(cfg)
+    rp = torch.empty(hi - lo + 1, dtype=torch.int64, device="cuda")
+    if gen == "stencil":
+        nat.check(nat.lib.spc5_gen_stencil27_box_rowptr(cfg["n"], nz, lo, hi, rp.data_ptr(), 0))
+    elif gen == "powerlaw":
+        table = torch.from_numpy(powerlaw_len_table()).to("cuda")
+        nat.check(nat.lib.spc5_gen_powerlaw_rowptr(PL_N, lo, hi, MATRIX_SEED, table.data_ptr(),
+                                                   PL_TABLE_BITS, rp.data_ptr(), 0))
+    else:
+        nat.check(nat.lib.spc5_gen_fem_rowptr(cfg["rows"] // 3, lo, hi, rp.data_ptr(), 0))
+    return rp
+
+
+def device_rows(cfg, lo: int, hi: int, rp=None):
+    """Device CSR (row_ptr, col_idx, values) of rows [lo, hi) of a config's
+    matrix (stencil / power-law / FEM): the twins of stencil27_rows /
+    powerlaw_rows / fem_rows, bit for bit."""
+    import torch
+
+    from . import _native as nat
+    gen, nz = _gen_args(cfg)
+    prec = cfg["precision"]
+    tdt = torch.float64 if prec == "f64" else torch.float32
+    pc = nat.F64 if prec == "f64" else nat.F32
+    if rp is None:
+        rp = device_rowptr(cfg, lo, hi)
+    nnz = int(rp[-1])
+    ci = torch.empty(max(nnz, 1), dtype=torch.int32, device="cuda")
+    va = torch.empty(max(nnz, 1), dtype=tdt, device="cuda")
+    if gen == "stencil":
+        nat.check(nat.lib.spc5_gen_stencil27_box_fill(cfg["n"], nz, lo, hi, pc, MATRIX_SEED,
+                                                      27.0, rp.data_ptr(), ci.data_ptr(),
+                                                      va.data_ptr(), 0))
+    elif gen == "powerlaw":
+        table = torch.from_numpy(powerlaw_len_table()).to("cuda")
+        nat.check(nat.lib.spc5_gen_powerlaw_fill(PL_N, lo, hi, pc, MATRIX_SEED,
+                                                 table.data_ptr(), PL_TABLE_BITS, rp.data_ptr(),
+                                                 ci.data_ptr(), va.data_ptr(), 0))
+    else:
+        nat.check(nat.lib.spc5_gen_fem_fill(cfg["rows"] // 3, lo, hi, pc, MATRIX_SEED,
+                                            rp.data_ptr(), ci.data_ptr(), va.data_ptr(), 0))
+    torch.cuda.synchronize()
+    return rp, ci[:nnz], va[:nnz]
+
+
+def host_rows(cfg, lo: int, hi: int) -> CsrMatrix:
+    """Host CSR of rows [lo, hi) of a config's matrix (numpy generators)."""
+    gen, nz = _gen_args(cfg)
+    if gen == "stencil":
+        return stencil27_rows(cfg["n"], lo, hi, cfg["precision"], nz=nz)
+    if gen == "powerlaw":
+        return powerlaw_rows(lo, hi, precision=cfg["precision"])
+    return fem_rows(lo, hi, precision=cfg["precision"])
+
+
+def config_shape(cfg) -> tuple[int, int]:
+    """(num_rows, num_cols) of a config's matrix."""
+    if "n" in cfg:
+        n = cfg["n"] ** 2 * cfg.get("nz", cfg["n"])
+        return n, n
+    if "rows" in cfg:
+        return cfg["rows"], cfg["cols"]
+    return 8192, 8192

@@ -12,7 +12,7 @@ import torch  # noqa: E402
 import bench  # noqa: E402
 from paper_2307_14774_b200 import _native as nat  # noqa: E402
 from paper_2307_14774_b200.blocks import torch_stream  # noqa: E402
-from paper_2307_14774_b200.workloads import CONFIGS, x_vector  # noqa: E402
+from paper_2307_14774_b200.workloads import CONFIGS  # noqa: E402
 
 fmts = [tuple(int(v) for v in f.split(",")) for f in
         (sys.argv[1] if len(sys.argv) > 1 else "1,8;2,8;4,8;8,8").split(";")]
@@ -20,8 +20,7 @@ reps = int(sys.argv[2]) if len(sys.argv) > 2 else 50
 cfg = int(sys.argv[3]) if len(sys.argv) > 3 else 2
 prec = CONFIGS[cfg]["precision"]
 tdt = torch.float64 if prec == "f64" else torch.float32
-mats, nr, nc = bench.build_matrices(cfg, fmts)
-x = torch.from_numpy(x_vector(nc, prec)).to("cuda")
+mats, nr, nc, x, _, _, _ = bench.build_matrices(cfg, fmts, validate=False)
 y = torch.empty(nr, dtype=tdt, device="cuda")
 out = {}
 for f in fmts:
@@ -37,5 +36,5 @@ for f in fmts:
     torch.cuda.synchronize()
     us = e0.elapsed_time(e1) * 1e3 / reps
     gbs = bench.alg_bytes(mats[f], 8 if prec == "f64" else 4) / us / 1e3
-    out[f"c{cfg}b{f}"] = [round(us, 1), round(gbs / 6468.6, 3)]
+    out[f"c{cfg}b{f}"] = [round(us, 1), round(gbs / bench.peaks()[0], 3)]
 print(json.dumps(out))
