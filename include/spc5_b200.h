@@ -24,11 +24,23 @@
  *      SPC5_EINDEX  -> IndexError   (set bit addresses a column >= num_cols;
  *                                    vlane.py:58-77)
  *      SPC5_ECUDA / SPC5_ENOMEM -> RuntimeError
- *  - A matrix handle may be used from several threads/streams at once
- *    (SPEC.md:373-374); the spmv path never allocates (a per-handle plan is
- *    built once, at construction/import).  The plan depends on the structure
- *    arrays (rowptr, colidx, masks) only: values may be rewritten in place
- *    between products, a structure change needs a new handle.
+ *  - A matrix handle may be used from several threads and streams at once
+ *    (SPEC.md:373-374): the plan is built once and then only read; products
+ *    on different streams use different scratch (carry slots of split
+ *    chunks, the device-resolved range of a range product), made on a
+ *    stream's first product; spc5_spmv_host calls on one handle are
+ *    serialised (one staging-buffer set per handle).  Products issued while
+ *    a stream is being captured into a CUDA graph use the handle's graph
+ *    scratch: replays of two graphs holding products of the same handle must
+ *    not overlap.
+ *  - Allocation: converted matrices are planned at construction; imported
+ *    ones by spc5_prepare or on their first product (which then validates,
+ *    allocates and synchronises).  spc5_prepare(m, stream) also makes that
+ *    stream's scratch, after which products on it never allocate or
+ *    synchronise and may be captured.  spc5_spmv_host allocates its staging
+ *    buffers on first use.  The plan depends on the structure arrays
+ *    (rowptr, colidx, masks) only: values may be rewritten in place between
+ *    products, a structure change needs a new handle.
  */
 #ifndef SPC5_B200_H
 #define SPC5_B200_H
@@ -133,7 +145,9 @@ int spc5_spmv_mirrored(spc5_matrix_t m, const void *d_x, void *d_y, double scale
  * Same product restricted to the panel range [panel_lo, panel_hi): rows
  * [panel_lo*r, min(panel_hi*r, num_rows)) of y are written, nothing else.
  * One worker of spmv_parallel (parallel.py:55-92); results are bitwise equal
- * to the full product's rows.
+ * to the full product's rows.  The range's block and chunk bounds are
+ * resolved on the device (a one-warp search launched before K2): no host
+ * synchronisation, capturable.
  */
 int spc5_spmv_panels(spc5_matrix_t m, int64_t panel_lo, int64_t panel_hi, const void *d_x,
                      void *d_y, int accumulate, void *stream);

@@ -6,7 +6,9 @@
 // thread-local message (spc5_last_error).
 #include <cuda_runtime.h>
 
+#include <atomic>
 #include <cstdio>
+#include <map>
 #include <mutex>
 #include <new>
 #include <string>
@@ -21,11 +23,34 @@ struct HostPipe {
     cudaEvent_t start = nullptr, done = nullptr, xin[8], yout[8];
 };
 
+// A handle: the matrix, its plan (built once, then read-only) and the
+// per-stream mutable scratch of its products.  Thread safety (header
+// contract): the plan is published through `ready` (acquire/release) under
+// plan_mu; products on different streams use different Scratch (carry slots,
+// device range), created on a stream's first product; the host-buffer
+// pipeline (one set of staging buffers and streams per handle) is serialised
+// by host_mu.
 struct spc5_matrix {
     spc5::Matrix m;
     std::mutex plan_mu;
+    std::atomic<bool> ready{false};
+    std::mutex scratch_mu;
+    std::map<cudaStream_t, spc5::Scratch> scratch;  // per stream
+    spc5::Scratch graph_scratch;  // products issued during stream capture
+    std::mutex host_mu;
     HostPipe pipe;
+    void free_scratch() {
+        for (auto &kv : scratch) {
+            spc5::dev_free(kv.second.carry);
+            spc5::dev_free(kv.second.range);
+        }
+        scratch.clear();
+        spc5::dev_free(graph_scratch.carry);
+        spc5::dev_free(graph_scratch.range);
+        graph_scratch = spc5::Scratch{};
+    }
     ~spc5_matrix() {
+        free_scratch();
         if (pipe.K) {
             cudaStreamDestroy(pipe.h2d);
             cudaStreamDestroy(pipe.d2h);
@@ -112,17 +137,60 @@ static void init_common(Matrix &m, int64_t num_rows, int64_t num_cols, int r, in
     cudaGetLastError();
 }
 
+static int alloc_scratch(const Matrix &m, Scratch *s) {
+    if (m.plan.num_split) SPC5_TRY(dev_alloc(&s->carry, (size_t)m.plan.num_chunks * m.r));
+    SPC5_TRY(dev_alloc(&s->range, 4));
+    return SPC5_OK;
+}
+
+// Builds the plan once (validating imported arrays) and the scratch used by
+// products issued during CUDA-graph capture (allocation is not capturable).
 static int ensure_plan(spc5_matrix *h, cudaStream_t st) {
-    if (h->m.plan.built) return SPC5_OK;
+    if (h->ready.load(std::memory_order_acquire)) return SPC5_OK;
     std::lock_guard<std::mutex> lk(h->plan_mu);
-    if (h->m.plan.built) return SPC5_OK;
-    int s = build_plan(h->m, /*validate=*/true, st);
+    if (h->ready.load(std::memory_order_relaxed)) return SPC5_OK;
+    int s = h->m.plan.built ? SPC5_OK : build_plan(h->m, /*validate=*/true, st);
+    if (s == SPC5_OK) s = alloc_scratch(h->m, &h->graph_scratch);
     if (s != SPC5_OK) {
         std::string keep = g_err;
         free_plan(h->m.plan);
+        h->free_scratch();
         g_err = keep;
+        return s;
     }
-    return s;
+    h->ready.store(true, std::memory_order_release);
+    return SPC5_OK;
+}
+
+// The scratch of products on stream `st`: one set per stream, so concurrent
+// products on different streams never share carry slots or range words
+// (products on one stream are ordered by the stream).  A stream under
+// capture gets the handle's graph scratch: replays of graphs holding
+// products of the same handle must not run concurrently.
+static int scratch_for(spc5_matrix *h, cudaStream_t st, Scratch *out) {
+    cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+    if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+        cudaGetLastError();
+        cs = cudaStreamCaptureStatusNone;
+    }
+    if (cs != cudaStreamCaptureStatusNone) {
+        *out = h->graph_scratch;
+        return SPC5_OK;
+    }
+    std::lock_guard<std::mutex> lk(h->scratch_mu);
+    auto it = h->scratch.find(st);
+    if (it == h->scratch.end()) {
+        Scratch s;
+        int rc = alloc_scratch(h->m, &s);
+        if (rc != SPC5_OK) {
+            dev_free(s.carry);
+            dev_free(s.range);
+            return rc;
+        }
+        it = h->scratch.emplace(st, s).first;
+    }
+    *out = it->second;
+    return SPC5_OK;
 }
 
 }  // namespace spc5
@@ -167,8 +235,10 @@ int spc5_convert_csr(int64_t num_rows, int64_t num_cols, int64_t nnz, int precis
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int s = convert_csr(m, d_row_ptr, d_col_idx, d_values, st);
     if (s == SPC5_OK) s = build_plan(m, /*validate=*/false, st);
+    if (s == SPC5_OK) s = ensure_plan(h, st);
     if (s != SPC5_OK) {
         std::string keep = g_err;
+        h->free_scratch();
         free_matrix(m);
         delete h;
         g_err = keep;
@@ -249,7 +319,10 @@ int spc5_info(spc5_matrix_t h, spc5_info_t *info) {
 int spc5_prepare(spc5_matrix_t h, void *stream) {
     if (!h) return fail(SPC5_EINVAL, "null handle");
     g_launches = 0;
-    return ensure_plan(h, static_cast<cudaStream_t>(stream));
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    SPC5_TRY(ensure_plan(h, st));
+    Scratch sc;  // this stream's scratch now, so its products never allocate
+    return scratch_for(h, st, &sc);
 }
 
 int spc5_export(spc5_matrix_t h, int64_t *rowptr, uint32_t *colidx, void *masks, void *values,
@@ -288,7 +361,9 @@ int spc5_spmv(spc5_matrix_t h, const void *d_x, void *d_y, int accumulate, void 
         return fail(SPC5_EINVAL, "x/y must be non-null");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     SPC5_TRY(ensure_plan(h, st));
-    return launch_spmv(h->m, 0, h->m.num_panels, d_x, d_y, accumulate, st);
+    Scratch sc;
+    SPC5_TRY(scratch_for(h, st, &sc));
+    return launch_spmv(h->m, 0, h->m.num_panels, d_x, d_y, accumulate, st, sc);
 }
 
 int spc5_spmv_mirrored(spc5_matrix_t h, const void *d_x, void *d_y, double scale,
@@ -306,7 +381,9 @@ int spc5_spmv_mirrored(spc5_matrix_t h, const void *d_x, void *d_y, double scale
     mi.scale = scale;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     SPC5_TRY(ensure_plan(h, st));
-    return launch_spmv(h->m, 0, h->m.num_panels, d_x, d_y, 0, st, &mi);
+    Scratch sc;
+    SPC5_TRY(scratch_for(h, st, &sc));
+    return launch_spmv(h->m, 0, h->m.num_panels, d_x, d_y, 0, st, sc, &mi);
 }
 
 int spc5_spmv_panels(spc5_matrix_t h, int64_t panel_lo, int64_t panel_hi, const void *d_x,
@@ -318,7 +395,9 @@ int spc5_spmv_panels(spc5_matrix_t h, int64_t panel_lo, int64_t panel_hi, const 
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     SPC5_TRY(ensure_plan(h, st));
     if (panel_lo == panel_hi) return SPC5_OK;
-    return launch_spmv(h->m, panel_lo, panel_hi, d_x, d_y, accumulate, st);
+    Scratch sc;
+    SPC5_TRY(scratch_for(h, st, &sc));
+    return launch_spmv(h->m, panel_lo, panel_hi, d_x, d_y, accumulate, st, sc);
 }
 
 // End-to-end product on host buffers, pipelined over PCIe: K nnz-balanced
@@ -339,8 +418,10 @@ int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, 
     const int vb = m.value_bytes();
     const size_t xb = (size_t)m.num_cols * vb, yb = (size_t)m.num_rows * vb;
     HostPipe &hp = h->pipe;
+    // one staging buffer pair and stream set per handle: concurrent host
+    // products of one handle run one after the other
+    std::lock_guard<std::mutex> host_lk(h->host_mu);
     {
-        std::lock_guard<std::mutex> lk(h->plan_mu);
         if (!m.dx) SPC5_TRY(dev_alloc(&m.dx, xb));
         if (!m.dy) SPC5_TRY(dev_alloc(&m.dy, yb));
         if (!hp.K) {
@@ -371,6 +452,8 @@ int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, 
     SPC5_CUDA(cudaStreamWaitEvent(hp.d2h, hp.start, 0));
     SPC5_CUDA(cudaStreamWaitEvent(hp.comp, hp.start, 0));
     cudaStream_t cs = hp.comp;  // products on the pipeline's own stream
+    Scratch sc;
+    SPC5_TRY(scratch_for(h, cs, &sc));
     int64_t have = 0;  // x columns already queued
     char *dx = static_cast<char *>(m.dx), *dy = static_cast<char *>(m.dy);
     const char *hx = static_cast<const char *>(h_x);
@@ -391,11 +474,11 @@ int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, 
         SPC5_CUDA(cudaEventRecord(hp.xin[k], hp.h2d));
         SPC5_CUDA(cudaStreamWaitEvent(cs, hp.xin[k], 0));
         if (hp.K == 1) {
-            SPC5_TRY(launch_spmv(m, 0, m.num_panels, m.dx, m.dy, accumulate, cs));
+            SPC5_TRY(launch_spmv(m, 0, m.num_panels, m.dx, m.dy, accumulate, cs, sc));
         } else {
             const int64_t blk[2] = {hp.b[k], hp.b[k + 1]};
-            SPC5_TRY(launch_spmv(m, hp.p[k], hp.p[k + 1], m.dx, m.dy, accumulate, cs, nullptr,
-                                 blk));
+            SPC5_TRY(launch_spmv(m, hp.p[k], hp.p[k + 1], m.dx, m.dy, accumulate, cs, sc,
+                                 nullptr, blk));
         }
         launches += g_launches;
         g_launches = 0;
@@ -440,6 +523,7 @@ int spc5_to_csr(spc5_matrix_t h, int64_t *d_row_ptr, int32_t *d_col_idx, void *d
 
 int spc5_free(spc5_matrix_t h) {
     if (!h) return SPC5_OK;
+    h->free_scratch();
     free_matrix(h->m);
     delete h;
     return SPC5_OK;

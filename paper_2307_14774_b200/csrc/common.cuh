@@ -38,6 +38,7 @@ struct Plan {
     int64_t split_len = 256;        // long panels are cut at global multiples of this
     int64_t max_chunk_blocks = 0, max_chunk_values = 0;
     int64_t max_lpp_panels = 0;     // panels of the largest lane-per-panel chunk
+    int64_t num_fvr = 0;            // flat value-range chunks (all of them: the FVR-only kernel)
     int64_t lay_rp = 0, lay_col = 0, lay_mask = 0, lay_val = 0;  // slot: hdr|bits|rec|col|mask|val
     int slot_bytes = 0;
     int64_t num_granules = 0;
@@ -103,9 +104,19 @@ struct Mirror {
     int64_t row0 = 0;
     double scale = 1.0;
 };
+// Per-call mutable device state of a product, one set per stream (capi.cu
+// scratch_for): the carry slots of split chunks and, for range products, the
+// device-resolved block/chunk range.  Calls on different streams never share
+// it, so one handle is safe under concurrent products.
+struct Scratch {
+    double *carry = nullptr;   // [num_chunks * r] when the plan has split chunks
+    int64_t *range = nullptr;  // [4]: b_lo, b_hi, c_lo, c_hi of a range product
+};
+// blk: the range's block bounds when the caller knows them (else they are
+// resolved on the device into scratch.range, with no host synchronisation)
 int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void *y,
-                int accumulate, cudaStream_t st, const Mirror *mirror = nullptr,
-                const int64_t *blk = nullptr);
+                int accumulate, cudaStream_t st, const Scratch &scratch,
+                const Mirror *mirror = nullptr, const int64_t *blk = nullptr);
 // host-buffer pipeline: K nnz-balanced panel stages, their block bounds and
 // the x prefix (columns) each stage reads
 int host_stages(const Matrix &m, int K, int64_t *p, int64_t *b, int64_t *need, cudaStream_t st);

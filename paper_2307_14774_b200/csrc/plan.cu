@@ -240,12 +240,14 @@ __global__ void pstart_bits_kernel(int64_t np, const int64_t *__restrict__ rowpt
 // combined by a butterfly), so short chunks still fill the warp; bit5 = in
 // that mode, the last panel continues into the next chunk
 constexpr int64_t kLppMinLanes = 24;  // panels * r * G
+__constant__ int fvr_dense_q = 4;  // FVR instead of LPP below fvr_dense_q/4 values per block row
 __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                                    const int64_t *__restrict__ chunk_b,
                                    const int64_t *__restrict__ chunk_p,
                                    const int64_t *__restrict__ rowptr,
                                    const int64_t *__restrict__ empty, int64_t ne, int lpr_split,
-                                   int lpr_bal_num, int lpr_bal_den, uint8_t *flags) {
+                                   int lpr_bal_num, int lpr_bal_den, int fvr,
+                                   const int64_t *__restrict__ chunk_v, uint8_t *flags) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
     uint8_t f = rowptr[chunk_p[c]] < chunk_b[c] ? 1 : 0;
@@ -277,6 +279,18 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                 maxlen * npc * lpr_bal_den <= lpr_bal_num * (cb1 - cb0) + 2 * lpr_bal_den * npc)
                 f |= 4 | (lg << 3) | (ends_clean ? 0 : 32);
         }
+        // flat value-range mode (bit6): fvr 1 (default) for the other
+        // chunks without empty panels when r >= 2 (for r = 1 the
+        // balanced-lane-range steps are cheaper) and for lane-per-panel
+        // chunks that are sparse (fewer than fvr_dense/4 values per block
+        // row: lane-per-panel-row lanes would mostly find empty rows); fvr 2:
+        // also r = 1; fvr 3: every chunk without empty panels.  Record fields
+        // limit a chunk to 4096 blocks and 8192 panels.
+        const int64_t nvals = chunk_v[c + 1] - chunk_v[c];
+        const bool sparse = nvals * 4 < (int64_t)fvr_dense_q * (cb1 - cb0) * r;
+        if (fvr >= 1 && cb1 - cb0 < 4096 && hi_p - lo_p < 8192 &&
+            ((f & 4) ? (sparse || fvr >= 3) : (r >= 2 || fvr >= 2)))
+            f = (f & 3) | 64;
     }
     flags[c] = f;
 }
@@ -291,7 +305,8 @@ __device__ __forceinline__ void blob_shape(int64_t b0, int64_t b1, int64_t npc, 
                                            int off32, int64_t *nwords, int64_t *nrec) {
     const bool lpr = flags & 4;
     *nwords = (!lpr && b1 > b0) ? ((b1 - 1 + off32) >> 5) - ((b0 + off32) >> 5) + 1 : 0;
-    *nrec = lpr ? npc * (1 << ((flags >> 3) & 3)) + 1 : 32;  // G sub-ranges per panel
+    // G sub-ranges per panel; scan modes 32 lane records (+ the value count in FVR mode)
+    *nrec = lpr ? npc * (1 << ((flags >> 3) & 3)) + 1 : ((flags & 64) ? 33 : 32);
 }
 __device__ __forceinline__ int64_t a16_dev(int64_t v) { return (v + 15) / 16 * 16; }
 
@@ -341,6 +356,47 @@ __global__ void blob_fill_kernel(int64_t nc, int r, int vs, int off32,
         const int64_t g0 = (b0 + off32) >> 5;
         for (int64_t i = lane; i < nw; i += 32) words[i] = pstart_bits[g0 + i];
         uint32_t *rec = reinterpret_cast<uint32_t *>(bl + rec_off);
+        if (f & 64) {
+            // flat value-range chunk: lane l of K2 owns the chunk's values
+            // [l*nv/32, (l+1)*nv/32); record = block holding its first value |
+            // set bits of that block before it << 12 | panel of that block << 19
+            // (relative to b0 / p0); rec[32] = nv
+            const int64_t n = b1 - b0;
+            const int64_t nv = chunk_v[c + 1] - chunk_v[c];
+            const int64_t sl = (lane * n) >> 5, el = ((lane + 1) * n) >> 5;
+            int cnt = 0;
+            for (int64_t b = sl; b < el; ++b)
+                for (int rr = 0; rr < r; ++rr) cnt += __popc(load_mask(masks, (b0 + b) * r + rr, vs));
+            int vin = cnt;
+            for (int d = 1; d < 32; d <<= 1) {
+                const int tv = __shfl_up_sync(0xffffffffu, vin, d);
+                if (lane >= d) vin += tv;
+            }
+            const int j = (int)((lane * nv) >> 5);
+            int k = 0;  // the lane whose block range holds value j
+            for (int d = 0; d < 32; ++d) k += __shfl_sync(0xffffffffu, vin, d) <= j ? 1 : 0;
+            const int excl = __shfl_sync(0xffffffffu, vin - cnt, min(k, 31));
+            int64_t b = ((int64_t)min(k, 31) * n) >> 5;
+            int run = excl, skip = 0;
+            for (; b < n; ++b) {
+                int cb = 0;
+                for (int rr = 0; rr < r; ++rr) cb += __popc(load_mask(masks, (b0 + b) * r + rr, vs));
+                if (run + cb > j) {
+                    skip = j - run;
+                    break;
+                }
+                run += cb;
+            }
+            // panel of block b: panel starts in chunk blocks 1 .. b
+            int starts = 0;
+            for (int64_t bb = 1; bb <= b; ++bb) {
+                const int64_t gb = b0 + bb + off32;
+                starts += (int)((pstart_bits[gb >> 5] >> (gb & 31)) & 1u);
+            }
+            rec[lane] = (uint32_t)b | ((uint32_t)skip << 12) | ((uint32_t)starts << 19);
+            if (lane == 0) rec[32] = (uint32_t)nv;
+            continue;
+        }
         if (!(f & 4)) {
             // scan-mode chunk: lane l of K2 owns blocks [l*n/32, (l+1)*n/32);
             // record = values before its first block | (panel starts in
@@ -431,8 +487,10 @@ __global__ void issue_rec_kernel(int64_t nc, int lb, int vb, const int64_t *__re
 
 // largest panel count of a lane-per-panel chunk (sizes the staged records)
 __global__ void lpp_panels_kernel(int64_t nc, const int64_t *__restrict__ chunk_p,
-                                  const uint8_t *__restrict__ flags, unsigned long long *out) {
+                                  const uint8_t *__restrict__ flags, unsigned long long *out,
+                                  unsigned long long *num_fvr) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < nc && (flags[c] & 64)) atomicAdd(num_fvr, 1ull);
     if (c < nc && (flags[c] & 4))
         atomicMax(out, (unsigned long long)((chunk_p[c + 1] - chunk_p[c] + ((flags[c] >> 5) & 1))
                                             << ((flags[c] >> 3) & 3)));
@@ -776,7 +834,9 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         if (!getenv("SPC5_CB_POW2") && avg >= 1.0) {
             int64_t kmax = (int64_t)((double)cb_max / ((double)lanes * avg));
             while (kmax > 1 && (double)(kmax * lanes) * avg * per_blk > (double)slot_cap) --kmax;
-            for (int64_t k = kmax; k >= 1; --k) {
+            // at most 8 panel-count candidates (each is a full build_chunks
+            // pass: bounded plan-build time on sparse matrices)
+            for (int64_t k = kmax; k >= 1 && targets.size() < 8; --k) {
                 targets.push_back({(int64_t)((double)(k * lanes) * avg), k * lanes});
                 // k-1 full steps and a 7/8-full last one, when k full ones
                 // just miss the slot (fp32 beta(2,16): 30 panels, not 16)
@@ -799,6 +859,16 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     // irregular r = 1 matrices (block-count targets): slots <= 8 KB
     int64_t irr_cap = m.r == 1 ? std::min<int64_t>(slot_cap, 8192) : slot_cap;
     if (const char *e = getenv("SPC5_SLOT_B_IRR")) irr_cap = std::max(1024, atoi(e));
+    // flat value-range chunks (knob SPC5_FVR: 0 off, 1 scan chunks of r >= 2
+    // and sparse lane-per-panel ones, 2 + scan chunks of r = 1, 3 every chunk
+    // without empty panels;
+    // SPC5_FVR_DENSE: values per block row below which LPP chunks go FVR, in quarters)
+    int fvr_mode = 1;
+    if (const char *e = getenv("SPC5_FVR")) fvr_mode = atoi(e);
+    if (const char *e = getenv("SPC5_FVR_DENSE")) {
+        const int q = atoi(e);
+        SPC5_CUDA(cudaMemcpyToSymbol(fvr_dense_q, &q, sizeof(int)));
+    }
     for (size_t ti = 0;; ++ti) {
         const int64_t cb = targets[ti].cb, ppc = targets[ti].ppc;
         SPC5_TRY(build_chunks(m, cb, ppc, st));
@@ -806,22 +876,23 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
             P.num_empty, getenv("SPC5_NO_LPR") ? -1 : (getenv("SPC5_LPR_SPLIT") ? 1 : 0),
-            lpr_bal, 4, P.chunk_flags);
+            lpr_bal, 4, fvr_mode, P.chunk_v, P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
-        unsigned long long *d_st = nullptr, h_st[3] = {0, 0, 0};
-        SPC5_TRY(dev_alloc(&d_st, 3));
-        SPC5_CUDA(cudaMemsetAsync(d_st, 0, 3 * sizeof(unsigned long long), st));
+        unsigned long long *d_st = nullptr, h_st[4] = {0, 0, 0, 0};
+        SPC5_TRY(dev_alloc(&d_st, 4));
+        SPC5_CUDA(cudaMemsetAsync(d_st, 0, 4 * sizeof(unsigned long long), st));
         chunk_stats_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, P.chunk_b, P.chunk_v, d_st);
         lpp_panels_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
-            P.num_chunks, P.chunk_p, P.chunk_flags, d_st + 2);
+            P.num_chunks, P.chunk_p, P.chunk_flags, d_st + 2, d_st + 3);
         SPC5_CUDA(cudaGetLastError());
-        SPC5_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, st));  // 4 counters
         SPC5_CUDA(cudaStreamSynchronize(st));
         dev_free(d_st);
         P.max_chunk_blocks = (int64_t)h_st[0];
         P.max_chunk_values = (int64_t)h_st[1];
         P.max_lpp_panels = (int64_t)h_st[2];
+        P.num_fvr = (int64_t)h_st[3];
         P.chunk_target = cb;
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
         const int64_t mb = P.max_chunk_blocks;
@@ -839,6 +910,9 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
                              128 * 128);
         const bool regular = !ppc || P.max_chunk_blocks * 4 <= cb * 5;
         const int64_t cap = ppc ? slot_cap : irr_cap;
+        if (!regular) {  // fewer panels per chunk only averages worse: go to block targets
+            while (ti + 1 < targets.size() && targets[ti + 1].ppc) ++ti;
+        }
         if (regular && (P.slot_bytes <= cap || cb == 1 || ti + 1 >= targets.size())) break;
         if (regular && cb <= 32 && P.slot_bytes <= 14 * 1024) break;
         free_chunks(P);

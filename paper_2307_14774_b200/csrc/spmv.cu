@@ -33,6 +33,7 @@
 #include <map>
 #include <mutex>
 #include <tuple>
+#include <type_traits>
 
 #include "common.cuh"
 
@@ -55,6 +56,7 @@ struct SpmvArgs {
     int64_t c_lo, c_hi;           // chunk index range
     int64_t b_lo, b_hi;           // blocks contributing to y
     int64_t p_lo, p_hi;           // panels whose rows may be written
+    const int64_t *range;         // range products: {b_lo, b_hi, c_lo, c_hi} resolved on the device
     double *carry;
     const int64_t *empty_panels;
     int64_t num_empty;
@@ -297,6 +299,7 @@ __device__ __forceinline__ void put_row(const SpmvArgs &a, T *y, int64_t row, do
     T sv = (T)(v * a.yscale);
     if (a.accumulate) sv = y[row] + sv;
     y[row] = sv;
+#pragma unroll 1  // (unrolled at every store site it bloats the hot loops out of the i-cache)
     for (int i = 0; i < a.nmirror; ++i) static_cast<T *>(a.mirror[i])[a.mirror_row0 + row] = sv;
 }
 template <typename T, int G>
@@ -1067,11 +1070,248 @@ __device__ __forceinline__ void blr_chunk(const SpmvArgs &a, int64_t c, int64_t 
     }
 }
 
+// shared-memory load that only happens when p (else `old` is kept)
+__device__ __forceinline__ uint32_t lds_u32_if(uint32_t addr, bool p, uint32_t old) {
+    uint32_t v = old;
+    asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}"
+                 : "+r"(v)
+                 : "r"(addr), "r"((int)p));
+    return v;
+}
+
+template <int LB>
+struct BlockBits {  // the R masks of one block, row-major, as one bit string
+    static constexpr int W = LB <= 8 ? 1 : 2;
+    using Word = typename std::conditional<(LB <= 4), uint32_t, uint64_t>::type;
+    Word w[W];
+    // (re)load when p
+    __device__ __forceinline__ void load_if(uint32_t addr, bool p) {
+        const int q = (int)p;
+        if constexpr (LB == 1) {
+            uint32_t v = w[0];
+            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u8 %0, [%1];\n}"
+                         : "+r"(v) : "r"(addr), "r"(q));
+            w[0] = v;
+        } else if constexpr (LB == 2) {
+            uint32_t v = w[0];
+            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u16 %0, [%1];\n}"
+                         : "+r"(v) : "r"(addr), "r"(q));
+            w[0] = v;
+        } else if constexpr (LB == 4) {
+            uint32_t v = w[0];
+            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}"
+                         : "+r"(v) : "r"(addr), "r"(q));
+            w[0] = v;
+        } else if constexpr (LB == 8) {  // 8-byte aligned: a block's masks start at b * LB
+            uint64_t v = w[0];
+            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u64 %0, [%1];\n}"
+                         : "+l"(v) : "r"(addr), "r"(q));
+            w[0] = v;
+        } else {
+            uint64_t v0 = w[0], v1 = w[1];
+            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.shared.v2.u64 {%0, %1}, [%2];\n}"
+                         : "+l"(v0), "+l"(v1) : "r"(addr), "r"(q));
+            w[0] = v0;
+            w[1] = v1;
+        }
+    }
+    __device__ __forceinline__ bool empty() const {
+        if constexpr (W == 1) return w[0] == 0;
+        else return (w[0] | w[1]) == 0;
+    }
+    __device__ __forceinline__ void take_if(bool p, const BlockBits &o) {
+#pragma unroll
+        for (int i = 0; i < W; ++i) w[i] = p ? o.w[i] : w[i];
+    }
+    // position of the lowest set bit (garbage when empty), cleared when p
+    __device__ __forceinline__ int pop_if(bool p) {
+        if constexpr (LB <= 4) {
+            const int q = __ffs(w[0]) - 1;
+            w[0] = p ? (w[0] & (w[0] - 1u)) : w[0];
+            return q;
+        } else if constexpr (W == 1) {
+            const int q = __ffsll((long long)w[0]) - 1;
+            w[0] = p ? (w[0] & (w[0] - 1ull)) : w[0];
+            return q;
+        } else {
+            const bool lo = w[0] != 0;
+            const uint64_t v = lo ? w[0] : w[1];
+            const int q = __ffsll((long long)v) - 1 + (lo ? 0 : 64);
+            const uint64_t c = v & (v - 1ull);
+            w[0] = (p && lo) ? c : w[0];
+            w[1] = (p && !lo) ? c : w[1];
+            return q;
+        }
+    }
+};
+
+// acc += v when p: a predicated add (an if-chain over a run-time row would be
+// folded by the compiler into an indexed add, moving the row sums to local memory)
+__device__ __forceinline__ void add_if(double &acc, double v, bool p) {
+    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q add.f64 %0, %0, %1;\n}"
+        : "+d"(acc)
+        : "d"(v), "r"((int)p));
+}
+
+#ifndef SPC5_FVR_U
+#define SPC5_FVR_U (R == 1 ? 8 : 4)
+#endif
+// Flat value-range mode (chunk flag bit6): lane l owns the chunk's values
+// [l*nv/32, (l+1)*nv/32) -- the same count for every lane, whatever the block
+// fill -- and walks them in storage order: a block's R masks form one
+// row-major bit string (the value order within a block), whose lowest set
+// bit gives the next value's row (bit / bits-per-row) and column (colidx +
+// bit % bits-per-row).  The plan's lane records give the block holding the
+// lane's first value, the set bits of that block before it and its panel.
+// The walk is branch-free: the next block's column start, masks and
+// panel-start bit are loaded one block ahead (predicated shared loads).  U
+// values per step: their x gathers are all issued before the first product.
+// Products go to R per-row sums of the current panel (predicated adds); a
+// block that starts a panel closes the current one exactly as in
+// balanced-lane-range mode (F for the panel open from the left, stores
+// otherwise) and one segmented warp scan per chunk joins panels that span
+// lanes.  For chunks of about one value per block row or fewer (power-law
+// rows, FEM beta(8,8)), where per-row modes mostly visit empty rows.
+template <typename T, typename MT, int R, bool GENERIC, int U>
+__device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int n,
+                                          bool head_mid, int sh0, uint32_t a_bits,
+                                          uint32_t a_rec, uint32_t a_col, uint32_t a_mask,
+                                          uint32_t a_val, int lane, const T *__restrict__ x,
+                                          T *__restrict__ y) {
+    constexpr int MB = (int)sizeof(MT);
+    constexpr int LB = R * MB;
+    constexpr int BPR = 8 * MB;  // bits per block row in the bit string
+    constexpr uint32_t SZ = (uint32_t)sizeof(T);
+    const uint32_t rec = lds_u32(a_rec + (uint32_t)lane * 4u);
+    const int nv = (int)lds_u32(a_rec + 128u);
+    const int j0 = (lane * nv) >> 5, j1 = ((lane + 1) * nv) >> 5;
+    const int V = j1 - j0;
+    const bool nonempty = V > 0;
+    int b = (int)(rec & 0xfffu);
+    const int skip = (int)((rec >> 12) & 0x7fu);
+    const int pf = (int)(rec >> 19);
+    int p = pf;
+    uint32_t col = lds_u32(a_col + (uint32_t)b * 4u);
+    BlockBits<LB> cur;
+    cur.w[0] = 0;
+    if constexpr (BlockBits<LB>::W == 2) cur.w[1] = 0;
+    cur.load_if(a_mask + (uint32_t)b * LB, true);
+    for (int k = 0; k < skip; ++k) cur.pop_if(true);
+    auto sbit = [&](int bb, uint32_t wrd) -> uint32_t { return (wrd >> ((sh0 + bb) & 31)) & 1u; };
+    auto sword = [&](int bb) -> uint32_t { return a_bits + (uint32_t)((sh0 + bb) >> 5) * 4u; };
+    // the lane's first value starts a panel (else the panel is open from the left)
+    const bool first_start = nonempty && skip == 0 && sbit(b, lds_u32(sword(b)));
+    const bool first_open = nonempty && !first_start;
+    // the next block, loaded ahead
+    int bn = min(b + 1, n - 1);
+    uint32_t ncol = lds_u32(a_col + (uint32_t)bn * 4u);
+    BlockBits<LB> nxt = cur;
+    nxt.load_if(a_mask + (uint32_t)bn * LB, true);
+    uint32_t nst = sbit(bn, lds_u32(sword(bn)));
+    uint32_t vaddr = a_val + (uint32_t)j0 * SZ;
+    double acc[R], F[R];
+#pragma unroll
+    for (int g = 0; g < R; ++g) acc[g] = F[g] = 0.0;
+    bool flushed = false;
+    const int vmax = (nv + 31) >> 5;
+    for (int s = 0; s < vmax; s += U) {
+        T xv[U], vv[U];
+        int rowk[U];
+        bool newp[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const bool valid = s + u < V;
+            const bool adv = valid && cur.empty();  // this value is the next block's first
+            b = adv ? bn : b;
+            col = adv ? ncol : col;
+            cur.take_if(adv, nxt);
+            newp[u] = adv && nst != 0;
+            bn = min(b + 1, n - 1);
+            ncol = lds_u32_if(a_col + (uint32_t)bn * 4u, adv, ncol);
+            nxt.load_if(a_mask + (uint32_t)bn * LB, adv);
+            const uint32_t wrd = lds_u32_if(sword(bn), adv, 0u);
+            nst = adv ? sbit(bn, wrd) : nst;
+            const int pos = cur.pop_if(valid);
+            rowk[u] = pos / BPR;
+            xv[u] = ldg_pred(x + (col + (uint32_t)(pos % BPR)), valid);
+            vv[u] = lds_pred<T>(vaddr + (uint32_t)u * SZ, valid);
+        }
+        vaddr += (uint32_t)U * SZ;
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            double pr;
+            if constexpr (sizeof(T) == 8) pr = (double)vv[u] * (double)xv[u];
+            else pr = (double)__fmul_rn((float)vv[u], (float)xv[u]);
+            if constexpr (R == 1) {
+                // a block starting a panel closes the current one: the lane's
+                // first close parks it in F when the panel was open from the left
+                const bool toF = newp[u] && !flushed && first_open;
+                const bool put = newp[u] && !toF &&
+                                 (!GENERIC || (p0 + p >= a.p_lo && p0 + p < a.p_hi));
+                F[0] = toF ? acc[0] : F[0];
+                if (put) blr_put<T, 1>(a, c, p0, p, head_mid, acc, y, false);
+                acc[0] = newp[u] ? pr : acc[0] + pr;
+                flushed = flushed || newp[u];
+                p += newp[u] ? 1 : 0;
+            } else {
+                if (newp[u]) {
+                    if (!flushed && first_open) {
+#pragma unroll
+                        for (int g = 0; g < R; ++g) F[g] = acc[g];
+                    } else {
+                        blr_put<T, R>(a, c, p0, p, head_mid, acc, y, GENERIC);
+                    }
+                    flushed = true;
+                    ++p;
+#pragma unroll
+                    for (int g = 0; g < R; ++g) acc[g] = 0.0;
+                }
+#pragma unroll
+                for (int g = 0; g < R; ++g) add_if(acc[g], pr, rowk[u] == g);
+            }
+        }
+    }
+    // join the panels that span lanes: segmented inclusive scan of L = acc
+    const bool seg = first_start || flushed;
+    const unsigned segs = __ballot_sync(kFull, seg) | 1u;
+    const unsigned lane_le = kFull >> (31 - lane);
+    const int segstart = 31 - __clz(segs & lane_le);
+#pragma unroll
+    for (int dd = 1; dd < 32; dd <<= 1) {
+        const bool take = lane - dd >= segstart;
+#pragma unroll
+        for (int g = 0; g < R; ++g) {
+            const double t = __shfl_up_sync(kFull, acc[g], dd);
+            if (take) acc[g] += t;
+        }
+    }
+    double prev[R];
+#pragma unroll
+    for (int g = 0; g < R; ++g) {
+        prev[g] = __shfl_up_sync(kFull, acc[g], 1);
+        if (lane == 0) prev[g] = 0.0;
+    }
+    if (nonempty) {
+        if (first_open && flushed) {  // the panel open from the left ends here
+            double v[R];
+#pragma unroll
+            for (int g = 0; g < R; ++g) v[g] = prev[g] + F[g];
+            blr_put<T, R>(a, c, p0, pf, head_mid, v, y, GENERIC);
+        } else if (first_start && j0 > 0) {  // it ended at this lane's boundary
+            blr_put<T, R>(a, c, p0, pf - 1, head_mid, prev, y, GENERIC);
+        }
+        if (lane == 31) blr_put<T, R>(a, c, p0, p, head_mid, acc, y, GENERIC);
+    }
+}
+
 // K2.  Each warp takes chunks c_lo + (blockIdx.x + k*gridDim.x)*W + warp,
 // k = 0, 1, ...; the CTA's warps work on neighbouring chunks (x reuse in L1).
 // GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
 // spmv_parallel); the arithmetic per panel is identical.
-template <typename T, typename MT, int R, bool GENERIC>
+// MODE 0: every chunk mode (per-chunk dispatch); MODE 1: flat value ranges
+// only (plans whose chunks are all FVR: the small hot loop stays in the
+// instruction cache)
+template <typename T, typename MT, int R, bool GENERIC, int MODE = 0>
 // 168 registers: 12 warps per SM (3 CTAs x 4 warps) fit the register file;
 // the shared-memory ring allows no more
 #ifndef SPC5_K2_MAXREG
@@ -1114,8 +1354,14 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
     const uint64_t pol = evict_first_policy();
     const int wpc = blockDim.x >> 5;  // warps per CTA
     const int64_t stride = (int64_t)gridDim.x * wpc;
-    const int64_t cfirst = a.c_lo + (int64_t)blockIdx.x * wpc + warp;
-    const int64_t c_end = a.c_hi;
+    int64_t c_lo = a.c_lo, c_end = a.c_hi, b_lo = a.b_lo, b_hi = a.b_hi;
+    if (GENERIC && a.range) {  // range resolved on the device by range_kernel
+        b_lo = a.range[0];
+        b_hi = a.range[1];
+        c_lo = a.range[2];
+        c_end = a.range[3];
+    }
+    const int64_t cfirst = c_lo + (int64_t)blockIdx.x * wpc + warp;
     // prologue: fill the ring with the warp's first S chunks
     if (lane == 0) {
         for (int i = 0; i < S; ++i) {
@@ -1147,8 +1393,8 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
         const int n = (int)(b1 - b0);
         int a0 = 0, a1 = n;  // blocks contributing to y
         if (GENERIC) {
-            a0 = (int)(max(b0, a.b_lo) - b0);
-            a1 = (int)(min(b1, a.b_hi) - b0);
+            a0 = (int)(max(b0, b_lo) - b0);
+            a1 = (int)(min(b1, b_hi) - b0);
         }
         // arrays are 256-byte aligned: a region's offset in its slot is its start mod 16
         const uint32_t a_bits = sbase + kHdr;  // words from granule (b0 + off32) >> 5
@@ -1158,9 +1404,15 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
         const uint32_t a_val = sbase + a.lay_val + (uint32_t)((v0 * (int64_t)sizeof(T)) & 15);
         const int sh0 = (int)((b0 + a.off32) & 31);
 
-        if (flags & 4) {  // lane-per-panel chunk
+        if (MODE == 1) {
+            fvr_chunk<T, MT, R, GENERIC, SPC5_FVR_U>(a, c, p0, n, head_mid, sh0, a_bits, a_rp,
+                                                     a_col, a_mask, a_val, lane, x, y);
+        } else if (flags & 4) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
                                          a_rp, a_col, a_mask, a_val, lane, x, y);
+        } else if (flags & 64) {  // flat value ranges
+            fvr_chunk<T, MT, R, GENERIC, SPC5_FVR_U>(a, c, p0, n, head_mid, sh0, a_bits, a_rp,
+                                                     a_col, a_mask, a_val, lane, x, y);
         } else if (!slow && SPC5_BLR) {  // balanced lane ranges
             blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, sbase + 48, a_bits,
                                                            a_rp, a_col, a_mask, a_val, lane, x, y);
@@ -1190,7 +1442,8 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
     const int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (i >= num_split) return;
     const int64_t c = split[i];
-    if (c < a.c_lo || c >= a.c_hi) return;
+    const int64_t c_lo = a.range ? a.range[2] : a.c_lo, c_hi = a.range ? a.range[3] : a.c_hi;
+    if (c < c_lo || c >= c_hi) return;
     const int64_t P = chunk_p[c];
     if (P < a.p_lo || P >= a.p_hi) return;
     if (i > 0 && split[i - 1] == c - 1 && chunk_p[c - 1] == P) return;  // not the first
@@ -1199,7 +1452,7 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
     for (int rr = 0; rr < R; ++rr) s[rr] = a.carry[c * R + rr];
     for (int64_t j = i + 1; j < num_split; ++j) {
         const int64_t cj = split[j];
-        if (cj != split[j - 1] + 1 || cj >= a.c_hi || chunk_p[cj] != P) break;
+        if (cj != split[j - 1] + 1 || cj >= c_hi || chunk_p[cj] != P) break;
 #pragma unroll
         for (int rr = 0; rr < R; ++rr) s[rr] += a.carry[cj * R + rr];
     }
@@ -1212,9 +1465,48 @@ __global__ void fixup_kernel(const int64_t *__restrict__ split, int64_t num_spli
         if (row < a.num_rows) {
             const T sv = y[row] + (T)(s[rr] * a.yscale);
             y[row] = sv;
+#pragma unroll 1
             for (int k = 0; k < a.nmirror; ++k)
                 static_cast<T *>(a.mirror[k])[a.mirror_row0 + row] = sv;
         }
+    }
+}
+
+// Number of entries of the sorted a[0, n) that are <= v (LE) or < v: a
+// 32-ary search by one warp, ~log32(n) rounds of one probe per lane.
+template <bool LE>
+__device__ int64_t warp_count(const int64_t *__restrict__ a, int64_t n, int64_t v, int lane) {
+    int64_t lo = 0, hi = n;  // the count is in [lo, hi]
+    while (hi - lo > 32) {
+        const int64_t step = (hi - lo + 31) / 32;
+        const int64_t i = lo + (int64_t)(lane + 1) * step - 1;
+        const bool ok = i < hi && (LE ? a[i] <= v : a[i] < v);
+        const int c = __popc(__ballot_sync(kFull, ok));  // probes that hold form a prefix
+        const int64_t nlo = min(hi, lo + (int64_t)c * step);
+        hi = min(hi, lo + (int64_t)(c + 1) * step - 1);
+        lo = nlo;
+    }
+    const int64_t i = lo + lane;
+    const bool ok = i < hi && (LE ? a[i] <= v : a[i] < v);
+    return lo + __popc(__ballot_sync(kFull, ok));
+}
+
+// Range products without a host round trip: the blocks of panels
+// [p_lo, p_hi) and the chunks holding them (as launch_spmv computes on the
+// host when the caller knows the block bounds).
+__global__ void range_kernel(const int64_t *__restrict__ rowptr, const int64_t *__restrict__ chunk_b,
+                             int64_t nc, int64_t p_lo, int64_t p_hi, int64_t *out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t blo = rowptr[p_lo], bhi = rowptr[p_hi];
+    int64_t clo = warp_count<true>(chunk_b, nc, blo, lane) - 1;
+    if (clo < 0) clo = 0;
+    int64_t chi = warp_count<false>(chunk_b, nc, bhi, lane);
+    if (blo >= bhi) chi = clo;  // no blocks: only empty-panel zeroing
+    if (lane == 0) {
+        out[0] = blo;
+        out[1] = bhi;
+        out[2] = clo;
+        out[3] = chi;
     }
 }
 
@@ -1279,7 +1571,10 @@ template <typename T, typename MT, int R>
 int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
     const Plan &P = m.plan;
     int launches = 1;
-    if (a.p_lo == 0 && a.p_hi == m.num_panels)
+    static const bool fvr_kernel = !getenv("SPC5_NO_FVR_KERNEL");
+    if (a.p_lo == 0 && a.p_hi == m.num_panels && P.num_fvr == P.num_chunks && fvr_kernel)
+        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 1>, m, a, a.c_hi - a.c_lo, st));
+    else if (a.p_lo == 0 && a.p_hi == m.num_panels)
         SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false>, m, a, a.c_hi - a.c_lo, st));
     else
         SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, a, a.c_hi - a.c_lo, st));
@@ -1306,7 +1601,8 @@ int dispatch_r(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
 }  // namespace
 
 int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void *y,
-                int accumulate, cudaStream_t st, const Mirror *mirror, const int64_t *blk) {
+                int accumulate, cudaStream_t st, const Scratch &scratch, const Mirror *mirror,
+                const int64_t *blk) {
     const Plan &P = m.plan;
     SpmvArgs a{};
     a.yscale = 1.0;
@@ -1333,7 +1629,8 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
     a.pstart_bits = P.pstart_bits;
     a.blob = P.blob;
     a.issue_rec = P.issue_rec;
-    a.carry = P.carry;
+    a.carry = scratch.carry;
+    if (P.num_split && !a.carry) return fail(SPC5_EINVAL, "no carry scratch for this stream");
     a.empty_panels = P.empty_panels;
     a.num_empty = P.num_empty;
     a.off32 = (int)(((m.block_base % 32) + 32) % 32);
@@ -1350,28 +1647,35 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
         a.b_lo = 0;
         a.b_hi = m.num_blocks;
     } else {
-        int64_t blo = 0, bhi = 0;
-        if (blk) {  // block range known to the caller: no round trip
-            blo = blk[0];
-            bhi = blk[1];
-        } else {
-            SPC5_CUDA(cudaMemcpyAsync(&blo, m.rowptr + p_lo, sizeof(int64_t),
-                                      cudaMemcpyDeviceToHost, st));
-            SPC5_CUDA(cudaMemcpyAsync(&bhi, m.rowptr + p_hi, sizeof(int64_t),
-                                      cudaMemcpyDeviceToHost, st));
-            SPC5_CUDA(cudaStreamSynchronize(st));
+        if (!blk && P.num_chunks) {
+            // block and chunk bounds resolved on the device (no host sync;
+            // capturable): the launch covers every chunk, warps past the
+            // resolved range exit at once
+            if (!scratch.range) return fail(SPC5_EINVAL, "no range scratch for this stream");
+            range_kernel<<<1, 32, 0, st>>>(m.rowptr, P.chunk_b, P.num_chunks, p_lo, p_hi,
+                                           scratch.range);
+            SPC5_CUDA(cudaGetLastError());
+            note_launches(1);
+            a.range = scratch.range;
+            a.c_lo = 0;
+            a.c_hi = P.num_chunks;
+            a.b_lo = 0;
+            a.b_hi = m.num_blocks;
+        } else if (blk) {  // block range known to the caller (host pipeline stages)
+            const int64_t blo = blk[0], bhi = blk[1];
+            a.b_lo = blo;
+            a.b_hi = bhi;
+            const int64_t *cb = P.h_chunk_b;
+            const int64_t nc = P.num_chunks;
+            a.c_lo = std::upper_bound(cb, cb + nc, blo) - cb - 1;
+            if (a.c_lo < 0) a.c_lo = 0;
+            a.c_hi = std::lower_bound(cb, cb + nc, bhi) - cb;
+            if (blo >= bhi) a.c_hi = a.c_lo;  // no blocks: only empty-panel zeroing
         }
-        a.b_lo = blo;
-        a.b_hi = bhi;
-        const int64_t *cb = P.h_chunk_b;
-        const int64_t nc = P.num_chunks;
-        a.c_lo = std::upper_bound(cb, cb + nc, blo) - cb - 1;
-        if (a.c_lo < 0) a.c_lo = 0;
-        a.c_hi = std::lower_bound(cb, cb + nc, bhi) - cb;
-        if (blo >= bhi) a.c_hi = a.c_lo;  // no blocks: only empty-panel zeroing
     }
     if (P.num_chunks == 0 || a.c_hi <= a.c_lo) {
         a.c_lo = a.c_hi = 0;
+        a.range = nullptr;
         if (accumulate || a.num_empty == 0) {
             note_launches(0);
             return SPC5_OK;
