@@ -238,6 +238,38 @@ int spc5_gen_fem_fill(int64_t nodes, int64_t row_lo, int64_t row_hi, int precisi
                       uint64_t seed, const int64_t *d_row_ptr, int32_t *d_col_idx,
                       void *d_values, void *stream);
 
+/*
+ * Multi-GPU row-panel sharding (one process per GPU, NCCL), the C-ABI form of
+ * spmv_parallel's partitioned product (parallel.py:55-92) and of BASELINE
+ * config 5's iterated loop.  NCCL (libnccl.so.2) is loaded on first use.
+ *
+ *  spc5_mg_unique_id   rank 0 makes the 128-byte NCCL id; the caller ships it
+ *                      to the other ranks (MPI, a file, torch.distributed...).
+ *  spc5_mg_init        one communicator per rank on the current CUDA device.
+ *  spc5_mg_partition   partition_by_nnz (parallel.py:31-52) of a CSR's panels
+ *                      from its DEVICE row pointers alone (int64[num_rows+1]):
+ *                      h_ranges = int64[2*workers] panel ranges (lo, hi),
+ *                      identical to the reference's for the converted matrix.
+ *  spc5_mg_shard       attach this rank's matrix (rows h_row_ranges[2*rank] ..
+ *                      h_row_ranges[2*rank+1] of a square matrix, converted on
+ *                      its own with spc5_convert_csr; borrowed, not freed);
+ *                      h_row_ranges = int64[2*nranks] ROW ranges of all ranks.
+ *  spc5_mg_spmv_step   x_next = scale * A . x: the local K2 writes this rank's
+ *                      rows of x_next, then one NCCL group of point-to-point
+ *                      sends/receives all-gathers the slices (unequal sizes),
+ *                      stream ordered.  x and x_next are full-length device
+ *                      vectors on every rank.
+ */
+typedef struct spc5_mg *spc5_mg_t;
+int spc5_mg_unique_id(void *id /* 128 bytes */);
+int spc5_mg_init(const void *id, int nranks, int rank, spc5_mg_t *out);
+int spc5_mg_partition(const int64_t *d_row_ptr, int64_t num_rows, int r, int workers,
+                      int64_t *h_ranges, void *stream);
+int spc5_mg_shard(spc5_mg_t mg, spc5_matrix_t local, const int64_t *h_row_ranges);
+int spc5_mg_spmv_step(spc5_mg_t mg, const void *d_x, void *d_x_next, double scale,
+                      void *stream);
+int spc5_mg_free(spc5_mg_t mg);
+
 /* Number of kernel launches the last spc5_spmv* call on this thread issued. */
 int spc5_last_launch_count(void);
 

@@ -71,6 +71,12 @@ SIGNATURES = {
                                _vp],
     "spc5_gen_fem_rowptr": [_i64, _i64, _i64, _vp, _vp],
     "spc5_gen_fem_fill": [_i64, _i64, _i64, _int, ctypes.c_uint64, _vp, _vp, _vp, _vp],
+    "spc5_mg_unique_id": [_vp],
+    "spc5_mg_init": [_vp, _int, _int, ctypes.POINTER(_vp)],
+    "spc5_mg_partition": [_vp, _i64, _int, _int, _vp, _vp],
+    "spc5_mg_shard": [_vp, _H, _vp],
+    "spc5_mg_spmv_step": [_vp, _vp, _vp, ctypes.c_double, _vp],
+    "spc5_mg_free": [_vp],
 }
 
 

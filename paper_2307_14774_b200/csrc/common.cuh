@@ -38,7 +38,8 @@ struct Plan {
     int64_t split_len = 256;        // long panels are cut at global multiples of this
     int64_t max_chunk_blocks = 0, max_chunk_values = 0;
     int64_t max_lpp_panels = 0;     // panels of the largest lane-per-panel chunk
-    int64_t num_fvr = 0;            // flat value-range chunks (all of them: the FVR-only kernel)
+    int64_t num_fvr = 0;            // flat value-range chunks (kernel variant choice)
+    int64_t num_lpp = 0;            // lane-per-panel-row chunks
     int64_t lay_rp = 0, lay_col = 0, lay_mask = 0, lay_val = 0;  // slot: hdr|bits|rec|col|mask|val
     int slot_bytes = 0;
     int64_t num_granules = 0;

@@ -488,9 +488,10 @@ __global__ void issue_rec_kernel(int64_t nc, int lb, int vb, const int64_t *__re
 // largest panel count of a lane-per-panel chunk (sizes the staged records)
 __global__ void lpp_panels_kernel(int64_t nc, const int64_t *__restrict__ chunk_p,
                                   const uint8_t *__restrict__ flags, unsigned long long *out,
-                                  unsigned long long *num_fvr) {
+                                  unsigned long long *num_fvr, unsigned long long *num_lpp) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c < nc && (flags[c] & 64)) atomicAdd(num_fvr, 1ull);
+    if (c < nc && (flags[c] & 4)) atomicAdd(num_lpp, 1ull);
     if (c < nc && (flags[c] & 4))
         atomicMax(out, (unsigned long long)((chunk_p[c + 1] - chunk_p[c] + ((flags[c] >> 5) & 1))
                                             << ((flags[c] >> 3) & 3)));
@@ -878,21 +879,22 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
             P.num_empty, getenv("SPC5_NO_LPR") ? -1 : (getenv("SPC5_LPR_SPLIT") ? 1 : 0),
             lpr_bal, 4, fvr_mode, P.chunk_v, P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
-        unsigned long long *d_st = nullptr, h_st[4] = {0, 0, 0, 0};
-        SPC5_TRY(dev_alloc(&d_st, 4));
-        SPC5_CUDA(cudaMemsetAsync(d_st, 0, 4 * sizeof(unsigned long long), st));
+        unsigned long long *d_st = nullptr, h_st[5] = {0, 0, 0, 0, 0};
+        SPC5_TRY(dev_alloc(&d_st, 5));
+        SPC5_CUDA(cudaMemsetAsync(d_st, 0, 5 * sizeof(unsigned long long), st));
         chunk_stats_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, P.chunk_b, P.chunk_v, d_st);
         lpp_panels_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
-            P.num_chunks, P.chunk_p, P.chunk_flags, d_st + 2, d_st + 3);
+            P.num_chunks, P.chunk_p, P.chunk_flags, d_st + 2, d_st + 3, d_st + 4);
         SPC5_CUDA(cudaGetLastError());
-        SPC5_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, st));  // 4 counters
+        SPC5_CUDA(cudaMemcpyAsync(h_st, d_st, sizeof(h_st), cudaMemcpyDeviceToHost, st));
         SPC5_CUDA(cudaStreamSynchronize(st));
         dev_free(d_st);
         P.max_chunk_blocks = (int64_t)h_st[0];
         P.max_chunk_values = (int64_t)h_st[1];
         P.max_lpp_panels = (int64_t)h_st[2];
         P.num_fvr = (int64_t)h_st[3];
+        P.num_lpp = (int64_t)h_st[4];
         P.chunk_target = cb;
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
         const int64_t mb = P.max_chunk_blocks;

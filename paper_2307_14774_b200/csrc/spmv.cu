@@ -1080,44 +1080,35 @@ __device__ __forceinline__ uint32_t lds_u32_if(uint32_t addr, bool p, uint32_t o
 }
 
 template <int LB>
-struct BlockBits {  // the R masks of one block, row-major, as one bit string
-    static constexpr int W = LB <= 8 ? 1 : 2;
-    using Word = typename std::conditional<(LB <= 4), uint32_t, uint64_t>::type;
-    Word w[W];
+struct BlockBits {  // the R masks of one block, row-major, as one bit string of 32-bit words
+    static constexpr int W = (LB + 3) / 4;
+    uint32_t w[W];
     // (re)load when p
     __device__ __forceinline__ void load_if(uint32_t addr, bool p) {
         const int q = (int)p;
         if constexpr (LB == 1) {
-            uint32_t v = w[0];
             asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u8 %0, [%1];\n}"
-                         : "+r"(v) : "r"(addr), "r"(q));
-            w[0] = v;
+                         : "+r"(w[0]) : "r"(addr), "r"(q));
         } else if constexpr (LB == 2) {
-            uint32_t v = w[0];
             asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u16 %0, [%1];\n}"
-                         : "+r"(v) : "r"(addr), "r"(q));
-            w[0] = v;
+                         : "+r"(w[0]) : "r"(addr), "r"(q));
         } else if constexpr (LB == 4) {
-            uint32_t v = w[0];
             asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}"
-                         : "+r"(v) : "r"(addr), "r"(q));
-            w[0] = v;
+                         : "+r"(w[0]) : "r"(addr), "r"(q));
         } else if constexpr (LB == 8) {  // 8-byte aligned: a block's masks start at b * LB
-            uint64_t v = w[0];
-            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u64 %0, [%1];\n}"
-                         : "+l"(v) : "r"(addr), "r"(q));
-            w[0] = v;
+            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.shared.v2.u32 {%0, %1}, [%2];\n}"
+                         : "+r"(w[0]), "+r"(w[1]) : "r"(addr), "r"(q));
         } else {
-            uint64_t v0 = w[0], v1 = w[1];
-            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %3, 0;\n @q ld.shared.v2.u64 {%0, %1}, [%2];\n}"
-                         : "+l"(v0), "+l"(v1) : "r"(addr), "r"(q));
-            w[0] = v0;
-            w[1] = v1;
+            asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %5, 0;\n"
+                         " @q ld.shared.v4.u32 {%0, %1, %2, %3}, [%4];\n}"
+                         : "+r"(w[0]), "+r"(w[1]), "+r"(w[2]), "+r"(w[3]) : "r"(addr), "r"(q));
         }
     }
     __device__ __forceinline__ bool empty() const {
-        if constexpr (W == 1) return w[0] == 0;
-        else return (w[0] | w[1]) == 0;
+        uint32_t o = w[0];
+#pragma unroll
+        for (int i = 1; i < W; ++i) o |= w[i];
+        return o == 0;
     }
     __device__ __forceinline__ void take_if(bool p, const BlockBits &o) {
 #pragma unroll
@@ -1125,32 +1116,41 @@ struct BlockBits {  // the R masks of one block, row-major, as one bit string
     }
     // position of the lowest set bit (garbage when empty), cleared when p
     __device__ __forceinline__ int pop_if(bool p) {
-        if constexpr (LB <= 4) {
+        if constexpr (W == 1) {
             const int q = __ffs(w[0]) - 1;
             w[0] = p ? (w[0] & (w[0] - 1u)) : w[0];
             return q;
-        } else if constexpr (W == 1) {
-            const int q = __ffsll((long long)w[0]) - 1;
-            w[0] = p ? (w[0] & (w[0] - 1ull)) : w[0];
-            return q;
         } else {
-            const bool lo = w[0] != 0;
-            const uint64_t v = lo ? w[0] : w[1];
-            const int q = __ffsll((long long)v) - 1 + (lo ? 0 : 64);
-            const uint64_t c = v & (v - 1ull);
-            w[0] = (p && lo) ? c : w[0];
-            w[1] = (p && !lo) ? c : w[1];
-            return q;
+            int k = W - 1;  // the first non-zero word
+#pragma unroll
+            for (int i = W - 2; i >= 0; --i) k = w[i] ? i : k;
+            uint32_t v = w[W - 1];
+#pragma unroll
+            for (int i = W - 2; i >= 0; --i) v = k == i ? w[i] : v;
+            const uint32_t cl = v & (v - 1u);
+#pragma unroll
+            for (int i = 0; i < W; ++i) w[i] = (p && k == i) ? cl : w[i];
+            return 32 * k + __ffs(v) - 1;
         }
     }
 };
 
-// acc += v when p: a predicated add (an if-chain over a run-time row would be
-// folded by the compiler into an indexed add, moving the row sums to local memory)
-__device__ __forceinline__ void add_if(double &acc, double v, bool p) {
-    asm("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q add.f64 %0, %0, %1;\n}"
-        : "+d"(acc)
-        : "d"(v), "r"((int)p));
+// acc[row] += v for a run-time row: R fused multiply-adds by a one-hot 1.0 /
+// 0.0 (3 instructions per row).  An if-chain is folded by the compiler into
+// an indexed add (row sums in local memory), a predicated add becomes an add
+// plus two selects.
+template <int R>
+__device__ __forceinline__ void add_row(double (&acc)[R], double v, int row) {
+    if constexpr (R == 1) {
+        acc[0] += v;
+    } else {
+#pragma unroll
+        for (int g = 0; g < R; ++g) {
+            // 1.0 has a zero low word: only the high word is selected
+            const double one_hot = __hiloint2double(row == g ? 0x3ff00000 : 0, 0);
+            acc[g] = fma(v, one_hot, acc[g]);
+        }
+    }
 }
 
 #ifndef SPC5_FVR_U
@@ -1176,12 +1176,11 @@ template <typename T, typename MT, int R, bool GENERIC, int U>
 __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int n,
                                           bool head_mid, int sh0, uint32_t a_bits,
                                           uint32_t a_rec, uint32_t a_col, uint32_t a_mask,
-                                          uint32_t a_val, int lane, const T *__restrict__ x,
+                                          const T *sval, int lane, const T *__restrict__ x,
                                           T *__restrict__ y) {
     constexpr int MB = (int)sizeof(MT);
     constexpr int LB = R * MB;
     constexpr int BPR = 8 * MB;  // bits per block row in the bit string
-    constexpr uint32_t SZ = (uint32_t)sizeof(T);
     const uint32_t rec = lds_u32(a_rec + (uint32_t)lane * 4u);
     const int nv = (int)lds_u32(a_rec + 128u);
     const int j0 = (lane * nv) >> 5, j1 = ((lane + 1) * nv) >> 5;
@@ -1193,52 +1192,70 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
     int p = pf;
     uint32_t col = lds_u32(a_col + (uint32_t)b * 4u);
     BlockBits<LB> cur;
-    cur.w[0] = 0;
-    if constexpr (BlockBits<LB>::W == 2) cur.w[1] = 0;
+#pragma unroll
+    for (int i = 0; i < BlockBits<LB>::W; ++i) cur.w[i] = 0;
     cur.load_if(a_mask + (uint32_t)b * LB, true);
     for (int k = 0; k < skip; ++k) cur.pop_if(true);
-    auto sbit = [&](int bb, uint32_t wrd) -> uint32_t { return (wrd >> ((sh0 + bb) & 31)) & 1u; };
-    auto sword = [&](int bb) -> uint32_t { return a_bits + (uint32_t)((sh0 + bb) >> 5) * 4u; };
+    // panel-start bits of the blocks after b (bit 0 = block b+1), refilled
+    // before a step that could walk past them
+    auto window = [&](int bb) -> uint32_t {  // start bits of blocks bb .. bb+31
+        const int g = sh0 + bb;
+        const uint32_t w0 = lds_u32(a_bits + (uint32_t)(g >> 5) * 4u);
+        const uint32_t w1 = lds_u32(a_bits + (uint32_t)((g >> 5) + 1) * 4u);
+        return __funnelshift_r(w0, w1, g & 31);
+    };
+    const uint32_t w_here = window(b);
     // the lane's first value starts a panel (else the panel is open from the left)
-    const bool first_start = nonempty && skip == 0 && sbit(b, lds_u32(sword(b)));
+    const bool first_start = nonempty && skip == 0 && (w_here & 1u);
     const bool first_open = nonempty && !first_start;
+    uint32_t sw = w_here >> 1;
+    int left = 31;  // valid bits in sw
     // the next block, loaded ahead
     int bn = min(b + 1, n - 1);
     uint32_t ncol = lds_u32(a_col + (uint32_t)bn * 4u);
     BlockBits<LB> nxt = cur;
     nxt.load_if(a_mask + (uint32_t)bn * LB, true);
-    uint32_t nst = sbit(bn, lds_u32(sword(bn)));
-    uint32_t vaddr = a_val + (uint32_t)j0 * SZ;
+    const T *vp = sval + j0;
     double acc[R], F[R];
 #pragma unroll
     for (int g = 0; g < R; ++g) acc[g] = F[g] = 0.0;
     bool flushed = false;
     const int vmax = (nv + 31) >> 5;
     for (int s = 0; s < vmax; s += U) {
+        if (left < U) {  // the start-bit window may run out in this step: refill (rare)
+            sw = window(b + 1);
+            left = 32;
+        }
         T xv[U], vv[U];
         int rowk[U];
         bool newp[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            if (s + u >= vmax) break;  // warp-uniform: the last step may be short
             const bool valid = s + u < V;
             const bool adv = valid && cur.empty();  // this value is the next block's first
             b = adv ? bn : b;
             col = adv ? ncol : col;
             cur.take_if(adv, nxt);
-            newp[u] = adv && nst != 0;
+            newp[u] = adv && (sw & 1u);
+            sw = adv ? sw >> 1 : sw;
+            left -= adv ? 1 : 0;
             bn = min(b + 1, n - 1);
             ncol = lds_u32_if(a_col + (uint32_t)bn * 4u, adv, ncol);
             nxt.load_if(a_mask + (uint32_t)bn * LB, adv);
-            const uint32_t wrd = lds_u32_if(sword(bn), adv, 0u);
-            nst = adv ? sbit(bn, wrd) : nst;
             const int pos = cur.pop_if(valid);
             rowk[u] = pos / BPR;
-            xv[u] = ldg_pred(x + (col + (uint32_t)(pos % BPR)), valid);
-            vv[u] = lds_pred<T>(vaddr + (uint32_t)u * SZ, valid);
+            xv[u] = T(0);
+            vv[u] = T(0);
+            if (valid) {
+                xv[u] = __ldg(x + (col + (uint32_t)(pos % BPR)));
+                vv[u] = vp[u];
+            }
         }
-        vaddr += (uint32_t)U * SZ;
+        vp += U;
 #pragma unroll
         for (int u = 0; u < U; ++u) {
+            if (s + u >= vmax) break;
             double pr;
             if constexpr (sizeof(T) == 8) pr = (double)vv[u] * (double)xv[u];
             else pr = (double)__fmul_rn((float)vv[u], (float)xv[u]);
@@ -1266,8 +1283,7 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
 #pragma unroll
                     for (int g = 0; g < R; ++g) acc[g] = 0.0;
                 }
-#pragma unroll
-                for (int g = 0; g < R; ++g) add_if(acc[g], pr, rowk[u] == g);
+                add_row<R>(acc, pr, rowk[u]);
             }
         }
     }
@@ -1308,10 +1324,13 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
 // k = 0, 1, ...; the CTA's warps work on neighbouring chunks (x reuse in L1).
 // GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
 // spmv_parallel); the arithmetic per panel is identical.
-// MODE 0: every chunk mode (per-chunk dispatch); MODE 1: flat value ranges
-// only (plans whose chunks are all FVR: the small hot loop stays in the
-// instruction cache)
-template <typename T, typename MT, int R, bool GENERIC, int MODE = 0>
+// Chunk modes compiled into a kernel (a plan whose chunks all use one or two
+// modes runs a kernel without the others' code: the hot loop stays small in
+// the instruction cache and the register allocation is its own).  MODE 0:
+// lane-per-panel-row, balanced lane ranges and lane-per-block (no flat value
+// ranges); 1: flat value ranges only; 2: every mode (mixed plans and range
+// products); 3: lane-per-panel-row only.
+template <typename T, typename MT, int R, bool GENERIC, int MODE>
 // 168 registers: 12 warps per SM (3 CTAs x 4 warps) fit the register file;
 // the shared-memory ring allows no more
 #ifndef SPC5_K2_MAXREG
@@ -1402,17 +1421,19 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
         const uint32_t a_col = sbase + a.lay_col + (uint32_t)((b0 * 4) & 15);
         const uint32_t a_mask = sbase + a.lay_mask + (uint32_t)((b0 * LB) & 15);
         const uint32_t a_val = sbase + a.lay_val + (uint32_t)((v0 * (int64_t)sizeof(T)) & 15);
+        // the same values through a typed pointer (compiler-visible shared loads)
+        const T *slot_values = reinterpret_cast<const T *>(smem + (a_val - smem_addr(smem)));
         const int sh0 = (int)((b0 + a.off32) & 31);
 
         if (MODE == 1) {
             fvr_chunk<T, MT, R, GENERIC, SPC5_FVR_U>(a, c, p0, n, head_mid, sh0, a_bits, a_rp,
-                                                     a_col, a_mask, a_val, lane, x, y);
-        } else if (flags & 4) {  // lane-per-panel chunk
+                                                     a_col, a_mask, slot_values, lane, x, y);
+        } else if (MODE == 3 || (flags & 4)) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
                                          a_rp, a_col, a_mask, a_val, lane, x, y);
-        } else if (flags & 64) {  // flat value ranges
+        } else if (MODE == 2 && (flags & 64)) {  // flat value ranges
             fvr_chunk<T, MT, R, GENERIC, SPC5_FVR_U>(a, c, p0, n, head_mid, sh0, a_bits, a_rp,
-                                                     a_col, a_mask, a_val, lane, x, y);
+                                                     a_col, a_mask, slot_values, lane, x, y);
         } else if (!slow && SPC5_BLR) {  // balanced lane ranges
             blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, sbase + 48, a_bits,
                                                            a_rp, a_col, a_mask, a_val, lane, x, y);
@@ -1571,13 +1592,19 @@ template <typename T, typename MT, int R>
 int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
     const Plan &P = m.plan;
     int launches = 1;
-    static const bool fvr_kernel = !getenv("SPC5_NO_FVR_KERNEL");
-    if (a.p_lo == 0 && a.p_hi == m.num_panels && P.num_fvr == P.num_chunks && fvr_kernel)
-        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 1>, m, a, a.c_hi - a.c_lo, st));
-    else if (a.p_lo == 0 && a.p_hi == m.num_panels)
-        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false>, m, a, a.c_hi - a.c_lo, st));
-    else
-        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true>, m, a, a.c_hi - a.c_lo, st));
+    const int64_t nc = a.c_hi - a.c_lo;
+    if (a.p_lo == 0 && a.p_hi == m.num_panels) {  // full product: the plan's modes only
+        if (P.num_fvr == P.num_chunks)
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 1>, m, a, nc, st));
+        else if (P.num_lpp == P.num_chunks)
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 3>, m, a, nc, st));
+        else if (P.num_fvr == 0)
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 0>, m, a, nc, st));
+        else
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 2>, m, a, nc, st));
+    } else {
+        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true, 2>, m, a, nc, st));
+    }
     if (P.num_split) {
         fixup_kernel<T, R><<<(unsigned)cdiv(P.num_split, 128), 128, 0, st>>>(
             P.split_chunks, P.num_split, P.chunk_p, a);

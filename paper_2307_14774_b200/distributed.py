@@ -29,7 +29,8 @@ from typing import Callable
 import numpy as np
 
 __all__ = ["panel_partition", "ShardLayout", "shard_layout", "allgather_slices",
-           "iterate_products", "FusedExchange", "iterate_products_fused", "bench_distributed"]
+           "iterate_products", "FusedExchange", "iterate_products_fused", "NcclShard",
+           "bench_distributed"]
 
 
 def panel_partition(row_ptr, r: int, workers: int) -> list[tuple[int, int]]:
@@ -194,6 +195,67 @@ def iterate_products_fused(x0, steps: int, layout: ShardLayout, rank: int, world
     return ex.run(handle, x0, steps, scale).clone()
 
 
+
+
+class NcclShard:
+    """This rank's shard of an iterated product through the C ABI's spc5_mg_*
+    entry points (NCCL driven from libspc5_b200.so, no torch.distributed on
+    the data path): ``step`` is x_next = scale * A.x, the local K2 into this
+    rank's rows of x_next, then the all-gather-v of the slices in one NCCL
+    group.  ``nccl_id`` is the 128-byte id of rank 0 (``NcclShard.unique_id()``),
+    shipped to the other ranks by any means."""
+
+    @staticmethod
+    def unique_id() -> bytes:
+        import ctypes
+
+        from . import _native as nat
+        buf = ctypes.create_string_buffer(128)
+        nat.check(nat.lib.spc5_mg_unique_id(buf))
+        return buf.raw
+
+    @staticmethod
+    def partition(row_ptr_dev, r: int, workers: int) -> list[tuple[int, int]]:
+        """partition_by_nnz panel ranges from device CSR row pointers (C ABI)."""
+        from . import _native as nat
+        from .blocks import torch_stream
+        out = np.zeros(2 * workers, dtype=np.int64)
+        nat.check(nat.lib.spc5_mg_partition(row_ptr_dev.data_ptr(), row_ptr_dev.numel() - 1, r,
+                                            workers, out.ctypes.data, torch_stream()))
+        return [(int(out[2 * k]), int(out[2 * k + 1])) for k in range(workers)]
+
+    def __init__(self, nccl_id: bytes, world: int, rank: int):
+        import ctypes
+
+        from . import _native as nat
+        self._nat = nat
+        self._h = ctypes.c_void_p()
+        nat.check(nat.lib.spc5_mg_init(ctypes.c_char_p(nccl_id), world, rank,
+                                       ctypes.byref(self._h)))
+        self.world, self.rank = world, rank
+        self._keep = None
+
+    def shard(self, matrix, layout: ShardLayout) -> None:
+        rows = np.array([v for k in range(self.world) for v in layout.rows(k)], dtype=np.int64)
+        self._keep = (matrix, rows)  # the C side borrows the matrix handle
+        self._nat.check(self._nat.lib.spc5_mg_shard(self._h, matrix.handle().ptr,
+                                                    rows.ctypes.data))
+
+    def step(self, x, x_next, scale: float = 1.0) -> None:
+        from .blocks import torch_stream
+        self._nat.check(self._nat.lib.spc5_mg_spmv_step(self._h, x.data_ptr(), x_next.data_ptr(),
+                                                        float(scale), torch_stream()))
+
+    def close(self) -> None:
+        if self._h:
+            self._nat.lib.spc5_mg_free(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
 
 
 # ----------------------------------------------------------------------------- bench

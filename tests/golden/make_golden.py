@@ -31,8 +31,8 @@ from pathlib import Path
 import numpy as np
 
 import spc5  # the reference package
-from spc5.blocks import VALID_R, VALID_VS, csr_to_spc5, filling_stats
-from spc5.kernels import csr_reference, spmv_spc5_scalar
+from spc5.blocks import VALID_R, VALID_VS, csr_to_spc5, filling_stats, footprint_comparison
+from spc5.kernels import block_value_offsets, csr_reference, mask_popcounts, spmv_spc5_scalar
 from spc5.mmio import CsrMatrix, make_dense, make_identity, make_random
 from spc5.parallel import partition_by_nnz
 from util import random_csr  # reference tests/util.py:41-51
@@ -77,10 +77,15 @@ def record(m, case_idx: int, full: bool, formats=None) -> dict:
                  "rowptr": digest(rp), "colidx": digest(ci), "masks": digest(mk),
                  "values": digest(va), "y_scalar": digest(y),
                  "filling": st.filling, "footprint_bytes": st.footprint_bytes,
-                 "partition": {str(w): partition_by_nnz(s, w).ranges for w in WORKERS}}
+                 "partition": {str(w): partition_by_nnz(s, w).ranges for w in WORKERS},
+                 # kernels.py:82-96 and blocks.py:192-198
+                 "offsets": digest(block_value_offsets(s)),
+                 "popcounts": digest(mask_popcounts(s.block_masks).astype(np.int64)),
+                 "footprint_comparison": list(footprint_comparison(m, r, vs))}
             if full:
                 f.update(rowptr_list=rp.tolist(), colidx_list=ci.tolist(),
-                         masks_list=mk.tolist(), values_list=va.tolist(), y_list=y.tolist())
+                         masks_list=mk.tolist(), values_list=va.tolist(), y_list=y.tolist(),
+                         offsets_list=block_value_offsets(s).tolist())
             rec["formats"][f"{r},{vs}"] = f
     return rec
 
@@ -148,6 +153,7 @@ def main():
                 "num_blocks": s.num_blocks, "rowptr": digest(rp), "colidx": digest(ci),
                 "masks": digest(mk), "values": digest(va), "y_scalar": digest(y),
                 "footprint_bytes": filling_stats(s).footprint_bytes,
+                "offsets": digest(block_value_offsets(s)),
                 "partition": {str(w): partition_by_nnz(s, w).ranges for w in (1, 2, 4, 8)}}
             print(f"config1 r={r} vs={vs} nb={s.num_blocks}", file=sys.stderr)
     (OUT / "config1.json").write_text(json.dumps(c1, indent=1))

@@ -149,3 +149,28 @@ def test_graph_capture_replay_bitwise(mats):
             g.replay()
             torch.cuda.synchronize()
             assert torch.equal(y, y0), key
+
+
+def test_c_abi_nccl_single_rank(cuda_device):
+    """spc5_mg_* on a one-rank NCCL communicator: the C-ABI partition equals
+    partition_by_nnz, and a step x_next = A.x/64 equals the plain product
+    scaled (the all-gather is empty at one rank)."""
+    import torch
+
+    import paper_2307_14774_b200 as spc5
+    from paper_2307_14774_b200.distributed import NcclShard, shard_layout
+    from paper_2307_14774_b200.workloads import stencil27, x_vector
+    m = stencil27(24)
+    rp = torch.from_numpy(m.row_ptr).cuda()
+    for r in (1, 2, 4, 8):
+        s = spc5.csr_to_spc5(m, r, 8)
+        for w in (1, 2, 3, 8):
+            assert NcclShard.partition(rp, r, w) == spc5.partition_by_nnz(s, w).ranges, (r, w)
+        mg = NcclShard(NcclShard.unique_id(), 1, 0)
+        mg.shard(s, shard_layout(m.row_ptr, r, 1))
+        x = torch.from_numpy(x_vector(m.num_cols)).cuda()
+        xn = torch.empty_like(x)
+        mg.step(x, xn, 1.0 / 64.0)
+        y = torch.from_numpy(spc5.spmv(s, x.cpu().numpy())).cuda() / 64.0
+        assert torch.equal(xn, y), r
+        mg.close()

@@ -1,0 +1,180 @@
+"""GPU entry points beside the product: validate_spc5's invariants with the
+reference's messages (blocks.py:201-232), block_value_offsets and
+footprint_comparison against the reference's outputs (tests/golden/), and the
+timing harness with the reference's test_bench.py semantics (run_bench
+validates before timing and refuses on failure, bench.py:153-184)."""
+
+import numpy as np
+import pytest
+
+from golden_io import Csr, digest, expected_small, fmt_keys, small_case, small_case_names
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def spc5(cuda_device):
+    import paper_2307_14774_b200 as pkg
+    return pkg
+
+
+def _hand_b24(spc5):
+    """The reference's hand matrix in beta(2,4) as host arrays (tests/test_blocks.py:30-36):
+    rowptr [0,2,3], colidx [0,6,6], masks [0b1101,0b0010,0b0001,0,0,0b0011], values 1..7."""
+    return dict(num_rows=4, num_cols=8, r=2, vs=4,
+                block_rowptr=np.array([0, 2, 3], np.int64),
+                block_colidx=np.array([0, 6, 6], np.uint32),
+                block_masks=np.array([0b1101, 0b0010, 0b0001, 0, 0, 0b0011], np.uint8),
+                values=np.arange(1.0, 8.0))
+
+
+# (how the arrays are corrupted, the message validate_spc5 raises, blocks.py:201-232)
+CORRUPTIONS = [
+    ("rowptr_len", "block_rowptr length does not match panel count"),
+    ("rowptr_dec", "block_rowptr must be non-decreasing and start at 0"),
+    ("rowptr_start", "block_rowptr must be non-decreasing and start at 0"),
+    ("rowptr_cover", "block_rowptr does not cover all blocks"),
+    ("mask_len", "mask array length must be num_blocks * r"),
+    ("bits_beyond_vs", "mask has bits beyond vs"),
+    ("popcount", "sum of mask popcounts differs from NNZ"),
+    ("anchor", "block without an entry at its anchor column"),
+    ("colidx_order", "panel 0: block columns not strictly increasing"),
+    ("past_last_col", "set mask bit maps past the last column"),
+]
+
+
+def _corrupt(d, how):
+    d = {k: (v.copy() if isinstance(v, np.ndarray) else v) for k, v in d.items()}
+    if how == "rowptr_len":
+        d["block_rowptr"] = np.array([0, 2, 3, 3], np.int64)
+    elif how == "rowptr_dec":
+        d["block_rowptr"] = np.array([0, 3, 2], np.int64)
+    elif how == "rowptr_start":
+        d["block_rowptr"] = np.array([1, 2, 3], np.int64)
+    elif how == "rowptr_cover":
+        d["block_rowptr"] = np.array([0, 2, 2], np.int64)
+    elif how == "mask_len":
+        d["block_masks"] = d["block_masks"][:5]
+    elif how == "bits_beyond_vs":
+        d["block_masks"][1] |= 0b10000  # bit 4 of a vs = 4 mask
+    elif how == "popcount":
+        d["block_masks"][5] = 0b0111
+    elif how == "anchor":  # same popcount, no entry at block 0's anchor column
+        d["block_masks"][0] = 0b1110
+    elif how == "colidx_order":
+        d["block_colidx"] = np.array([6, 0, 6], np.uint32)
+    elif how == "past_last_col":
+        d["block_colidx"] = np.array([0, 6, 7], np.uint32)  # bit 1 of block 2 -> column 8
+    return d
+
+
+def test_validate_accepts_valid(spc5):
+    d = _hand_b24(spc5)
+    spc5.validate_spc5(spc5.Spc5Matrix(**d))
+    m = small_case("hand")
+    for r in (1, 2, 4, 8):
+        for vs in (4, 8, 16):
+            spc5.validate_spc5(spc5.csr_to_spc5(m, r, vs))
+
+
+@pytest.mark.parametrize("how,msg", CORRUPTIONS)
+def test_validate_invariants_reference_messages(spc5, how, msg):
+    d = _corrupt(_hand_b24(spc5), how)
+    with pytest.raises(ValueError) as e:
+        spc5.validate_spc5(spc5.Spc5Matrix(**d))
+    assert str(e.value) == msg
+
+
+@pytest.mark.parametrize("name", small_case_names())
+def test_block_value_offsets_golden(spc5, name):
+    m = small_case(name)
+    rec = expected_small()["cases"][name]
+    for r, vs, f in fmt_keys(rec):
+        s = spc5.csr_to_spc5(m, r, vs)
+        off = spc5.block_value_offsets(s)
+        assert digest(off.astype(np.int64)) == f["offsets"], (name, r, vs)
+        assert int(off[-1]) == m.nnz
+        if "offsets_list" in f:
+            assert off.tolist() == f["offsets_list"]
+
+
+@pytest.mark.parametrize("name", ["hand", "edge", "tall", "rand03", "rand11", "longrows"])
+def test_footprint_comparison_golden(spc5, name):
+    m = small_case(name)
+    rec = expected_small()["cases"][name]
+    for r, vs, f in fmt_keys(rec):
+        assert list(spc5.footprint_comparison(m, r, vs)) == f["footprint_comparison"], (r, vs)
+
+
+# ---- harness (the reference's tests/test_bench.py semantics) ------------------
+def test_run_bench_identity(spc5):
+    m = spc5.make_identity(256)
+    rec = spc5.run_bench("identity:256", m, 1, 8, spc5.KernelConfig(), reps=5, warmup=1)
+    assert rec.reps == 5 and rec.median_seconds > 0
+    assert rec.gflops == 2 * 256 / rec.median_seconds / 1e9
+    assert rec.nnz == 256
+
+
+def test_run_bench_grid_cardinality(spc5):
+    m = spc5.make_random(32, 32, 4, 0.5, seed=1)
+    records = [spc5.run_bench("m", m, 1, 8, spc5.KernelConfig(strategy=st, reduction=rd),
+                              reps=2, warmup=1)
+               for st in ("expand", "compact") for rd in ("hsum", "multi")]
+    assert len({(r.strategy, r.reduction) for r in records}) == 4
+
+
+def test_run_bench_refuses_on_failed_validation(spc5, monkeypatch):
+    import paper_2307_14774_b200.harness as harness
+
+    def always_fail(*args, **kwargs):
+        return spc5.VerifyReport(passed=False, max_scaled_error=99.0, threshold=8.0,
+                                 worst_row=3, worst_trial=0, trials=1)
+
+    monkeypatch.setattr(harness, "verify_against_oracle", always_fail)
+    with pytest.raises(spc5.ValidationError, match="worst row 3"):
+        spc5.run_bench("m", spc5.make_identity(8), 1, 8, spc5.KernelConfig(), reps=1, warmup=0)
+
+
+def test_run_bench_refuses_corrupted_conversion(spc5, monkeypatch):
+    """A conversion that drops a mask bit must not be timed (bench.py:163-167)."""
+    import paper_2307_14774_b200.harness as harness
+    real = harness.csr_to_spc5
+
+    def broken(m, r, vs):
+        s = real(m, r, vs)
+        d = dict(num_rows=s.num_rows, num_cols=s.num_cols, r=s.r, vs=s.vs,
+                 block_rowptr=s.block_rowptr.copy(), block_colidx=s.block_colidx.copy(),
+                 block_masks=s.block_masks.copy(), values=s.values.copy())
+        d["values"][0] += 1.0  # wrong matrix: the product disagrees with the oracle
+        return spc5.Spc5Matrix(**d)
+
+    monkeypatch.setattr(harness, "csr_to_spc5", broken)
+    with pytest.raises(spc5.ValidationError):
+        spc5.run_bench("m", spc5.make_random(64, 64, 4, 0.5, seed=3), 2, 8, spc5.KernelConfig(),
+                       reps=1, warmup=0)
+
+
+def test_run_kernel_parallel_dispatch(spc5):
+    m = spc5.make_random(64, 64, 4, 0.5, seed=2)
+    s = spc5.csr_to_spc5(m, 2, 8)
+    x = np.ones(64)
+    y1 = np.zeros(64)
+    spc5.run_kernel(s, x, y1, spc5.KernelConfig(), workers=1)
+    y4 = np.zeros(64)
+    res = spc5.run_kernel(s, x, y4, spc5.KernelConfig(), workers=4)
+    assert y1.tobytes() == y4.tobytes()
+    assert res.elapsed >= 0 and res.flops == 2 * m.nnz
+
+
+def test_time_device_spmv(spc5):
+    from paper_2307_14774_b200.harness import time_device_spmv
+    s = spc5.csr_to_spc5(spc5.make_random(4096, 4096, 16, 0.5, seed=4), 4, 8)
+    t = time_device_spmv(s, reps=5, warmup=2)
+    assert len(t) == 5 and all(v > 0 for v in t)
+
+
+def test_csr_type_duck(spc5):
+    """Any object with the CsrMatrix fields converts (reference mmio.py:84-100 names)."""
+    m = small_case("hand")
+    s = spc5.csr_to_spc5(Csr(m.num_rows, m.num_cols, m.row_ptr, m.col_idx, m.values), 2, 4)
+    assert s.block_colidx.tolist() == [0, 6, 6]

@@ -508,53 +508,6 @@ def _full_config_parity(spc5, cfg_id):
 
 
 @pytest.mark.slow
-def test_config5_row_slices(spc5):
-    """BASELINE config 5 (stencil 400^3, 64M rows, 1.73G nnz) at full size on one
-    GPU, f64 and f32: device generator -> K1 -> K2; rows of three slices (start,
-    middle, end) checked against the oracle on host-generated rows, and y's
-    checksum against the exact GPU verifier over all rows."""
-    import torch
-    from paper_2307_14774_b200 import _native as nat
-    from paper_2307_14774_b200.workloads import stencil27_nnz, stencil27_rows, x_vector
-    from paper_2307_14774_b200.blocks import csr_to_spc5_device
-    n = 400
-    N = n ** 3
-    for prec, r, vs in (("f64", 1, 8), ("f32", 2, 16)):
-        tdt = torch.float64 if prec == "f64" else torch.float32
-        rp = torch.empty(N + 1, dtype=torch.int64, device="cuda")
-        nat.check(nat.lib.spc5_gen_stencil27_rowptr(n, 0, N, rp.data_ptr(), 0))
-        nnz = int(rp[-1])
-        assert nnz == stencil27_nnz(n)
-        ci = torch.empty(nnz, dtype=torch.int32, device="cuda")
-        va = torch.empty(nnz, dtype=tdt, device="cuda")
-        nat.check(nat.lib.spc5_gen_stencil27_fill(n, 0, N, 1 if prec == "f64" else 0, 0, 27.0,
-                                                  rp.data_ptr(), ci.data_ptr(), va.data_ptr(), 0))
-        torch.cuda.synchronize()
-        s = csr_to_spc5_device(N, N, rp, ci, va, r, vs)
-        x = torch.from_numpy(x_vector(N, prec)).to("cuda")
-        y = torch.empty(N, dtype=tdt, device="cuda")
-        nat.check(nat.lib.spc5_spmv(s.handle().ptr, x.data_ptr(), y.data_ptr(), 0, 0))
-        ye = torch.empty(N, dtype=torch.float64, device="cuda")
-        ya = torch.empty(N, dtype=torch.float64, device="cuda")
-        nat.check(nat.lib.spc5_csr_exact(N, 1 if prec == "f64" else 0, rp.data_ptr(),
-                                         ci.data_ptr(), va.data_ptr(), x.data_ptr(),
-                                         ye.data_ptr(), ya.data_ptr(), 0))
-        err = ((y.to(torch.float64) - ye).abs() / ya.clamp(min=1e-300)).max().item()
-        assert err <= TOL[prec], (prec, err)
-        del ci, va, rp
-        xh, yh = x.cpu().numpy(), y.cpu().numpy()
-        for lo in (0, N // 2 - 1000, N - 3000):
-            m = stencil27_rows(n, lo, lo + 3000, prec)
-            ys = np.zeros(m.num_rows, dtype=xh.dtype)
-            oracle.spmv_spc5_scalar(oracle.csr_to_spc5(m, r, vs), xh, ys)
-            _, a = oracle.csr_reference(m, xh)
-            e = oracle.relative_error(yh[lo:lo + 3000], ys, a)
-            assert float(e.max()) <= TOL[prec], (prec, lo, float(e.max()))
-        del s, x, y, ye, ya
-        torch.cuda.empty_cache()
-
-
-@pytest.mark.slow
 def test_config3_full_size(spc5):
     """BASELINE config 3: power-law 4,194,304^2, f32, beta(1|2|4, 16)."""
     _full_config_parity(spc5, 3)

@@ -155,3 +155,21 @@ def test_unsorted_csr_rejected():
     bad = Csr(1, 8, np.array([0, 2], np.int64), np.array([5, 3], np.int32), np.ones(2))
     with pytest.raises(ValueError):
         oracle.csr_to_spc5(bad, 1, 8)
+
+
+def test_offsets_and_popcounts_golden():
+    """oracle.block_value_offsets and the package's host mask_popcounts against the
+    reference's block_value_offsets / mask_popcounts (kernels.py:82-96), and the
+    footprint comparison formula (blocks.py:192-198)."""
+    import paper_2307_14774_b200 as spc5
+    for name in small_case_names():
+        m = small_case(name)
+        for r, vs, f in fmt_keys(expected_small()["cases"][name]):
+            s = oracle.csr_to_spc5(m, r, vs)
+            assert digest(oracle.block_value_offsets(s)) == f["offsets"], (name, r, vs)
+            assert digest(spc5.mask_popcounts(s.block_masks)) == f["popcounts"], (name, r, vs)
+            vb = m.values.dtype.itemsize
+            csr_bytes = (m.num_rows + 1) * 4 + m.nnz * 4 + m.nnz * vb
+            spc5_bytes = (m.nnz * vb + s.num_blocks * 4 + s.num_blocks * r * (1 if vs <= 8 else 2)
+                          + (s.num_panels + 1) * 4)
+            assert [csr_bytes, spc5_bytes] == f["footprint_comparison"], (name, r, vs)

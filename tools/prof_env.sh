@@ -14,4 +14,6 @@ for item in $1; do
   echo "$tag rc=$?"
   ncu -i /tmp/prof/$tag.ncu-rep --page raw --csv > $O/$tag.raw.csv 2>/dev/null
   python tools/ncu_stalls.py /tmp/prof/$tag.ncu-rep spmv_kernel 40 > $O/$tag.stalls.txt 2>&1
+  ncu -i /tmp/prof/$tag.ncu-rep --page source --csv --print-source sass > $O/$tag.sass.csv 2>/dev/null
+  gzip -f $O/$tag.sass.csv
 done
