@@ -290,7 +290,7 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
         const bool sparse = nvals * 4 < (int64_t)fvr_dense_q * (cb1 - cb0) * r;
         if (fvr >= 1 && cb1 - cb0 < 4096 && hi_p - lo_p < 8192 &&
             ((f & 4) ? (sparse || fvr >= 3) : (r >= 2 || fvr >= 2)))
-            f = (f & 3) | 64;
+            f = (f & 3) | 64 | ((f & 4) ? 0 : 128);  // bit7: was a scan chunk
     }
     flags[c] = f;
 }
@@ -483,6 +483,52 @@ __global__ void issue_rec_kernel(int64_t nc, int lb, int vb, const int64_t *__re
     B.w = 0;
     ir[2 * c] = A;
     ir[2 * c + 1] = B;
+}
+
+// x leading edge of every chunk, for the L2 prefetch K2 issues when it
+// queues the chunk's bulk copies: xmax[c] = the end of the columns chunk c
+// reads (max over its blocks of colidx + vs, clipped); the new x of chunk c
+// is [xmax[c-1], xmax[c]) -- for banded matrices walked in row order that is
+// the band's leading edge, first read by this chunk.  Encoded into the issue
+// record's last word (B.w): start | sectors << 27 in 32-byte sectors (at most
+// 31 sectors, the nearest part of the range; 0 = no prefetch: the range is
+// empty, goes backwards, or x is past 4 GB).
+__global__ void chunk_xmax_kernel(int64_t nc, const int64_t *__restrict__ chunk_b,
+                                  const uint32_t *__restrict__ colidx, int vs, int64_t num_cols,
+                                  int64_t *xmax) {
+    const int lane = threadIdx.x & 31;
+    const int64_t warp = (blockIdx.x * (int64_t)blockDim.x + threadIdx.x) >> 5;
+    const int64_t nw = ((int64_t)gridDim.x * blockDim.x) >> 5;
+    for (int64_t c = warp; c < nc; c += nw) {
+        int64_t mx = 0;
+        for (int64_t b = chunk_b[c] + lane; b < chunk_b[c + 1]; b += 32)
+            mx = max(mx, min((int64_t)colidx[b] + vs, num_cols));
+        for (int o = 16; o; o >>= 1) mx = max(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        if (lane == 0) xmax[c] = mx;
+    }
+}
+
+__global__ void xedge_kernel(int64_t nc, const int64_t *__restrict__ xmax, int vb, uint4 *ir) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= nc) return;
+    const int64_t hi = xmax[c] * vb, lo = c ? xmax[c - 1] * vb : 0;  // bytes
+    uint32_t w = 0;
+    if (hi > lo && hi <= (int64_t(1) << 32)) {
+        const int64_t s1 = hi >> 5;                        // whole sectors inside x only
+        const int64_t s0 = max(lo >> 5, s1 - 31);          // at most 31 sectors
+        if (s1 > s0) w = (uint32_t)s0 | ((uint32_t)(s1 - s0) << 27);
+    }
+    ir[2 * c + 1].w = w;
+}
+
+// scan chunks of a mostly lane-per-panel plan go back to balanced lane ranges
+// (bit7 -> clear bit6): the kernel without the FVR code then runs the plan
+__global__ void unfvr_kernel(int64_t nc, uint8_t *flags, unsigned long long *cleared) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c < nc && (flags[c] & 128)) {
+        flags[c] &= (uint8_t)~(64 | 128);
+        atomicAdd(cleared, 1ull);
+    }
 }
 
 // largest panel count of a lane-per-panel chunk (sizes the staged records)
@@ -895,6 +941,21 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.max_lpp_panels = (int64_t)h_st[2];
         P.num_fvr = (int64_t)h_st[3];
         P.num_lpp = (int64_t)h_st[4];
+        // a plan that is mostly lane-per-panel chunks (regular stencil-like
+        // matrices) keeps its few scan chunks in balanced-lane-range mode:
+        // the FVR code would otherwise be compiled into its kernel
+        if (fvr_mode < 2 && P.num_fvr && P.num_lpp * 2 > P.num_chunks) {
+            unsigned long long *d_cl = nullptr, h_cl = 0;
+            SPC5_TRY(dev_alloc(&d_cl, 1));
+            SPC5_CUDA(cudaMemsetAsync(d_cl, 0, sizeof(unsigned long long), st));
+            unfvr_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(P.num_chunks,
+                                                                            P.chunk_flags, d_cl);
+            SPC5_CUDA(cudaGetLastError());
+            SPC5_CUDA(cudaMemcpyAsync(&h_cl, d_cl, sizeof(h_cl), cudaMemcpyDeviceToHost, st));
+            SPC5_CUDA(cudaStreamSynchronize(st));
+            dev_free(d_cl);
+            P.num_fvr -= (int64_t)h_cl;
+        }
         P.chunk_target = cb;
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
         const int64_t mb = P.max_chunk_blocks;
@@ -956,6 +1017,18 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         issue_rec_kernel<<<(unsigned)cdiv(nc, 256), 256, 0, st>>>(
             nc, m.r * m.mask_bytes(), m.value_bytes(), P.chunk_b, P.chunk_v, off16, P.issue_rec);
         SPC5_CUDA(cudaGetLastError());
+        // (not for f64 beta(8,8): issue-bound there, 3482 -> 3560 us on the 400^3 stencil)
+        if (!getenv("SPC5_NO_XPREFETCH") && !(m.r == 8 && m.value_bytes() == 8)) {
+            int64_t *xmax = nullptr;
+            SPC5_TRY(dev_alloc(&xmax, (size_t)nc));
+            chunk_xmax_kernel<<<(unsigned)std::min<int64_t>(cdiv(nc, 8), 148 * 32), 256, 0, st>>>(
+                nc, P.chunk_b, m.colidx, m.vs, m.num_cols, xmax);
+            xedge_kernel<<<(unsigned)cdiv(nc, 256), 256, 0, st>>>(nc, xmax, m.value_bytes(),
+                                                                  P.issue_rec);
+            SPC5_CUDA(cudaGetLastError());
+            SPC5_CUDA(cudaStreamSynchronize(st));
+            dev_free(xmax);
+        }
         SPC5_CUDA(cudaStreamSynchronize(st));
         dev_free(size16);
         dev_free(off16);

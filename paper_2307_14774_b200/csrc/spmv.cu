@@ -74,6 +74,7 @@ struct SpmvArgs {
     int64_t mirror_row0;
     double yscale;
     int plain;  // !accumulate && !nmirror && yscale == 1
+    int x_prefetch;  // x is 16-byte aligned: the chunks' x leading edges are prefetched to L2
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -457,9 +458,24 @@ __device__ __forceinline__ void row_dispatch_sep(double (&acc)[U], uint32_t (&m)
 // with bulk copies completing on one mbarrier: its metadata blob (header,
 // panel-start words or panel records), column starts, masks and values.
 // The plan precomputed every source offset and size (16-byte units).
+#ifndef SPC5_X_PREFETCH
+#define SPC5_X_PREFETCH 1
+#endif
+// L2 prefetch of x (the chunk's new columns, plan.cu xedge_kernel): issued
+// with the chunk's bulk copies, a ring slot ahead of the chunk's x gathers, so
+// the first reads of a banded matrix's leading edge hit L2 instead of DRAM
+__device__ __forceinline__ void prefetch_x(const SpmvArgs &a, uint32_t w) {
+    if (w) {
+        const uint8_t *p = static_cast<const uint8_t *>(a.x) + (size_t)(w & 0x7ffffffu) * 32;
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"((w >> 27) * 32u)
+                     : "memory");
+    }
+}
+
 template <typename T, int LB>
 __device__ __forceinline__ void issue_chunk(const SpmvArgs &a, uint4 A, uint4 B, uint32_t slot,
                                             uint64_t *bar, uint64_t pol) {
+    if (SPC5_X_PREFETCH && a.x_prefetch) prefetch_x(a, B.w);
     const uint8_t *colb = reinterpret_cast<const uint8_t *>(a.colidx);
     const uint8_t *maskb = static_cast<const uint8_t *>(a.masks);
     const uint8_t *valb = static_cast<const uint8_t *>(a.values);
@@ -1709,6 +1725,7 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
         }
     }
     a.plain = !accumulate && a.nmirror == 0 && a.yscale == 1.0;
+    a.x_prefetch = (reinterpret_cast<uintptr_t>(x) & 15) == 0;
     const bool f64 = m.precision == SPC5_F64;
     const bool wide = m.vs > 8;
     if (f64) return wide ? dispatch_r<double, uint16_t>(m, a, st) : dispatch_r<double, uint8_t>(m, a, st);

@@ -36,8 +36,13 @@ for ln in open(sassf):
     if not infn:
         continue
     if "//##" in ln:
-        m = re.search(r'line (\d+)', ln)
-        cur = int(m.group(1)) if m and srcf.split("/")[-1] in ln else None
+        m = re.search(r'File "([^"]+)", line (\d+)', ln)
+        if m and srcf.split("/")[-1] in m.group(1):
+            cur = int(m.group(2))
+        elif m:
+            cur = m.group(1).split("/")[-1] + ":" + m.group(2)
+        else:
+            cur = None
         continue
     m = re.match(r'\s+/\*([0-9a-f]{4,})\*/\s+\S', ln)
     if m:
@@ -51,5 +56,5 @@ for off, e in execd.items():
 te, ts = sum(E.values()), sum(S.values()) or 1
 print(f"total warp instructions executed {te:.4g}; unmapped {E[None]:.3g}")
 for ln, e in E.most_common(top):
-    s = src[ln - 1].strip()[:70] if ln else "?"
+    s = src[ln - 1].strip()[:70] if isinstance(ln, int) else (ln or "?")
     print(f"{ln!s:>5} {e / te:6.1%} {S[ln] / ts:6.1%}  {s}")
