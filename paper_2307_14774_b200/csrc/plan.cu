@@ -972,7 +972,9 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
                              128 * 128);
         const bool regular = !ppc || P.max_chunk_blocks * 4 <= cb * 5;
-        const int64_t cap = ppc ? slot_cap : irr_cap;
+        // FVR kernels of r = 8 keep their row sums in shared memory (r*256 B
+        // per warp = r*128 B per ring slot): smaller slots keep 3 CTAs per SM
+        const int64_t cap = (ppc ? slot_cap : irr_cap) - (P.num_fvr && m.r == 8 ? m.r * 128 : 0);
         if (!regular) {  // fewer panels per chunk only averages worse: go to block targets
             while (ti + 1 < targets.size() && targets[ti + 1].ppc) ++ti;
         }

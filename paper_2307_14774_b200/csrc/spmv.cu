@@ -75,6 +75,7 @@ struct SpmvArgs {
     double yscale;
     int plain;  // !accumulate && !nmirror && yscale == 1
     int x_prefetch;  // x is 16-byte aligned: the chunks' x leading edges are prefetched to L2
+    uint32_t acc_off;  // FVR kernels with R = 8: per-warp row sums in shared memory (R*256 B)
 };
 
 constexpr unsigned kFull = 0xffffffffu;
@@ -1136,6 +1137,13 @@ struct BlockBits {  // the R masks of one block, row-major, as one bit string of
             const int q = __ffs(w[0]) - 1;
             w[0] = p ? (w[0] & (w[0] - 1u)) : w[0];
             return q;
+        } else if constexpr (W == 2) {
+            const bool lo = w[0] != 0u;
+            const uint32_t v = lo ? w[0] : w[1];
+            const uint32_t cl = v & (v - 1u);
+            w[0] = (p && lo) ? cl : w[0];
+            w[1] = (p && !lo) ? cl : w[1];
+            return (lo ? 0 : 32) + __ffs(v) - 1;
         } else {
             int k = W - 1;  // the first non-zero word
 #pragma unroll
@@ -1235,6 +1243,17 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
     double acc[R], F[R];
 #pragma unroll
     for (int g = 0; g < R; ++g) acc[g] = F[g] = 0.0;
+    // R = 8: the row sums of the current panel live in shared memory (row g
+    // of this lane at sacc[g*32 + lane]): one load-add-store per value
+    // instead of R one-hot fused multiply-adds
+    constexpr bool SACC = R == 8;  // (measured: R = 4 is faster with one-hot adds)
+    double *sacc = nullptr;  // row sums of this lane, stride 32
+    if constexpr (SACC) {
+        extern __shared__ __align__(128) uint8_t smem_dyn[];
+        sacc = reinterpret_cast<double *>(smem_dyn + a.acc_off) + (threadIdx.x >> 5) * (R * 32) + lane;
+#pragma unroll
+        for (int g = 0; g < R; ++g) sacc[g * 32] = 0.0;
+    }
     bool flushed = false;
     const int vmax = (nv + 31) >> 5;
     for (int s = 0; s < vmax; s += U) {
@@ -1287,7 +1306,17 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
                 flushed = flushed || newp[u];
                 p += newp[u] ? 1 : 0;
             } else {
-                if (newp[u]) {
+                // a block starting a panel closes the current one; the
+                // warp-uniform test keeps the rare close a real branch (the
+                // compiler would otherwise predicate its whole body into every step)
+                if (newp[u]) {  // a block starting a panel: close the current one
+                    if constexpr (SACC) {
+#pragma unroll
+                        for (int g = 0; g < R; ++g) {
+                            acc[g] = sacc[g * 32];
+                            sacc[g * 32] = 0.0;
+                        }
+                    }
                     if (!flushed && first_open) {
 #pragma unroll
                         for (int g = 0; g < R; ++g) F[g] = acc[g];
@@ -1299,9 +1328,14 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
 #pragma unroll
                     for (int g = 0; g < R; ++g) acc[g] = 0.0;
                 }
-                add_row<R>(acc, pr, rowk[u]);
+                if constexpr (SACC) sacc[rowk[u] * 32] += pr;
+                else add_row<R>(acc, pr, rowk[u]);
             }
         }
+    }
+    if constexpr (SACC) {
+#pragma unroll
+        for (int g = 0; g < R; ++g) acc[g] = sacc[g * 32];
     }
     // join the panels that span lanes: segmented inclusive scan of L = acc
     const bool seg = first_start || flushed;
@@ -1549,7 +1583,7 @@ __global__ void range_kernel(const int64_t *__restrict__ rowptr, const int64_t *
 
 template <typename K>
 int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
-                       cudaStream_t st) {
+                       cudaStream_t st, int acc_per_warp = 0) {
     // 4 warps per CTA: with 168 registers per thread three CTAs share an SM
     // tuning knobs, read once per process: SPC5_WPC (warps per CTA), SPC5_NSLOT
     static const int env_wpc = [] {
@@ -1563,7 +1597,9 @@ int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
     int wpc = env_wpc ? env_wpc : 4;
     const int S = env_nslot;
     a.nslot = S;
-    const size_t smem = kRingOff + (size_t)wpc * S * a.lay_bytes;  // barriers + ring
+    // barriers + ring (+ the FVR row sums of R >= 4 kernels)
+    a.acc_off = kRingOff + (uint32_t)(wpc * S) * a.lay_bytes;
+    const size_t smem = kRingOff + (size_t)wpc * S * a.lay_bytes + (size_t)wpc * acc_per_warp;
     // launch shape per (kernel, warps, shared memory), computed once: the
     // attribute/occupancy queries cost more host time than a launch
     int per_sm = 0;
@@ -1609,17 +1645,18 @@ int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
     const Plan &P = m.plan;
     int launches = 1;
     const int64_t nc = a.c_hi - a.c_lo;
+    constexpr int ACC = R == 8 ? R * 256 : 0;  // FVR row sums per warp (kernels with FVR code)
     if (a.p_lo == 0 && a.p_hi == m.num_panels) {  // full product: the plan's modes only
         if (P.num_fvr == P.num_chunks)
-            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 1>, m, a, nc, st));
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 1>, m, a, nc, st, ACC));
         else if (P.num_lpp == P.num_chunks)
             SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 3>, m, a, nc, st));
         else if (P.num_fvr == 0)
             SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 0>, m, a, nc, st));
         else
-            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 2>, m, a, nc, st));
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 2>, m, a, nc, st, ACC));
     } else {
-        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true, 2>, m, a, nc, st));
+        SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true, 2>, m, a, nc, st, ACC));
     }
     if (P.num_split) {
         fixup_kernel<T, R><<<(unsigned)cdiv(P.num_split, 128), 128, 0, st>>>(
