@@ -392,7 +392,21 @@ def ours_single(args, formats):
         b = alg_bytes(mats[f], vb)
         tot_bytes += b
         tot_time += t
+        # K1 (conversion) device time and its algorithmic bytes: the CSR read by
+        # each pass (count: row_ptr + col_idx; fill: row_ptr + col_idx + values)
+        # plus the SPC5 arrays written
+        ct = mats[f].handle().convert_timing()
+        nnz, nb = mats[f].nnz, mats[f].num_blocks
+        k1_bytes = (2 * (8 * num_rows + 4 * nnz) + vb * nnz          # CSR in, both passes
+                    + 8 * (mats[f].num_panels + 1) + 4 * nb           # rowptr, colidx out
+                    + nb * f[0] * (1 if f[1] <= 8 else 2) + vb * nnz)  # masks, values out
+        k1_ms = ct["k1_count_ms"] + ct["k1_fill_ms"]
+        conv = {"k1_ms": k1_ms, "k1_count_ms": ct["k1_count_ms"], "k1_fill_ms": ct["k1_fill_ms"],
+                "plan_ms": ct["plan_ms"], "k1_alg_bytes": k1_bytes,
+                "k1_gbs": k1_bytes / k1_ms / 1e6 if k1_ms > 0 else None,
+                "k1_frac": k1_bytes / k1_ms / 1e6 / peak if k1_ms > 0 else None}
         fmts[fmt_key(*f)] = {"us": t * 1e6, "gflops": 2.0 * mats[f].nnz / t / 1e9,
+                             "conversion": conv,
                              "alg_bytes": b, "gbs": b / t / 1e9, "frac": b / t / 1e9 / peak,
                              "nnz": mats[f].nnz, "num_blocks": mats[f].num_blocks,
                              **validation.get(fmt_key(*f), {})}

@@ -106,6 +106,16 @@ int spc5_import(int64_t num_rows, int64_t num_cols, int r, int vs, int precision
 int spc5_info(spc5_matrix_t m, spc5_info_t *info);
 
 /*
+ * Device times (CUDA events, ms) of the spc5_convert_csr call that built m:
+ * the K1 count pass, the K1 fill pass (incl. the r = 1 value copy) and the
+ * SpMV plan build.  Zeros for imported matrices.  Measurement only; the
+ * reference times conversion with perf_counter around csr_to_spc5
+ * (bench.py:158-160).
+ */
+int spc5_convert_timing(spc5_matrix_t m, double *k1_count_ms, double *k1_fill_ms,
+                        double *plan_ms);
+
+/*
  * Build the SpMV plan now (validating imported arrays, status mapping above).
  * Converted matrices are planned at construction; imported ones on their
  * first product or here.  After it returns, spc5_spmv never allocates or

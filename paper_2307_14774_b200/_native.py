@@ -43,6 +43,8 @@ SIGNATURES = {
     "spc5_device_count": [ctypes.POINTER(_int)],
     "spc5_convert_csr": [_i64, _i64, _i64, _int, _int, _int, _vp, _vp, _vp, _i64, _vp,
                          ctypes.POINTER(_H)],
+    "spc5_convert_timing": [_H, ctypes.POINTER(ctypes.c_double), ctypes.POINTER(ctypes.c_double),
+                            ctypes.POINTER(ctypes.c_double)],
     "spc5_import": [_i64, _i64, _int, _int, _int, _i64, _i64, _vp, _vp, _vp, _vp, _int, _i64,
                     _vp, ctypes.POINTER(_H)],
     "spc5_info": [_H, ctypes.POINTER(Spc5Info)],

@@ -100,6 +100,13 @@ class _Handle:
     def refresh(self):
         nat.check(nat.lib.spc5_info(self.ptr, ctypes.byref(self.info)))
 
+    def convert_timing(self) -> dict:
+        """Device times (ms) of the K1 conversion that built this matrix."""
+        a, b, c = ctypes.c_double(), ctypes.c_double(), ctypes.c_double()
+        nat.check(nat.lib.spc5_convert_timing(self.ptr, ctypes.byref(a), ctypes.byref(b),
+                                              ctypes.byref(c)))
+        return {"k1_count_ms": a.value, "k1_fill_ms": b.value, "plan_ms": c.value}
+
     def __del__(self):
         try:
             if self.ptr:

@@ -234,7 +234,18 @@ int spc5_convert_csr(int64_t num_rows, int64_t num_cols, int64_t nnz, int precis
     m.nnz = nnz;
     cudaStream_t st = static_cast<cudaStream_t>(stream);
     int s = convert_csr(m, d_row_ptr, d_col_idx, d_values, st);
-    if (s == SPC5_OK) s = build_plan(m, /*validate=*/false, st);
+    if (s == SPC5_OK) {
+        cudaEvent_t p0 = nullptr, p1 = nullptr;
+        cudaEventCreate(&p0);
+        cudaEventCreate(&p1);
+        cudaEventRecord(p0, st);
+        s = build_plan(m, /*validate=*/false, st);
+        cudaEventRecord(p1, st);
+        if (s == SPC5_OK && cudaEventSynchronize(p1) == cudaSuccess)
+            cudaEventElapsedTime(&m.plan_ms, p0, p1);
+        cudaEventDestroy(p0);
+        cudaEventDestroy(p1);
+    }
     if (s == SPC5_OK) s = ensure_plan(h, st);
     if (s != SPC5_OK) {
         std::string keep = g_err;
@@ -313,6 +324,15 @@ int spc5_info(spc5_matrix_t h, spc5_info_t *info) {
     // blocks.py:180-183 (4-byte declared index width)
     info->footprint_bytes = m.nnz * m.value_bytes() + m.num_blocks * 4 +
                             m.num_blocks * m.r * m.mask_bytes() + (m.num_panels + 1) * 4;
+    return SPC5_OK;
+}
+
+int spc5_convert_timing(spc5_matrix_t h, double *k1_count_ms, double *k1_fill_ms,
+                        double *plan_ms) {
+    if (!h) return fail(SPC5_EINVAL, "null handle");
+    if (k1_count_ms) *k1_count_ms = h->m.k1_count_ms;
+    if (k1_fill_ms) *k1_fill_ms = h->m.k1_fill_ms;
+    if (plan_ms) *plan_ms = h->m.plan_ms;
     return SPC5_OK;
 }
 

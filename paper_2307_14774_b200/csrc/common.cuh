@@ -62,6 +62,10 @@ struct Matrix {
     // scratch of the host-buffer path
     void *dx = nullptr, *dy = nullptr;
     int sm_count = 148;
+    // CUDA-event times of the conversion that built this matrix (ms; 0 for
+    // imported matrices): K1 count pass, K1 fill pass (+ the r = 1 value
+    // copy), plan build -- spc5_convert_timing
+    float k1_count_ms = 0.f, k1_fill_ms = 0.f, plan_ms = 0.f;
 
     int mask_bytes() const { return vs <= 8 ? 1 : 2; }
     int value_bytes() const { return precision == SPC5_F64 ? 8 : 4; }

@@ -243,8 +243,19 @@ int convert_csr(Matrix &m, const int64_t *d_row_ptr, const int32_t *d_col_idx,
     int64_t *counts = nullptr;
     SPC5_TRY(dev_alloc(&counts, (size_t)np));
     a.panel_blocks = counts;
+    struct Events {  // destroyed on every exit path
+        cudaEvent_t e[4] = {};
+        ~Events() {
+            for (auto &x : e)
+                if (x) cudaEventDestroy(x);
+        }
+    } evs;
+    cudaEvent_t *ev = evs.e;
+    for (int i = 0; i < 4; ++i) SPC5_CUDA(cudaEventCreate(&ev[i]));
+    SPC5_CUDA(cudaEventRecord(ev[0], st));
     launch_convert<false>(m.r, a, st);
     SPC5_CUDA(cudaGetLastError());
+    SPC5_CUDA(cudaEventRecord(ev[1], st));
     SPC5_TRY(inclusive_scan<int64_t>(counts, m.rowptr + 1, np, st));
     dev_free(counts);
     int64_t nb = 0;
@@ -258,11 +269,16 @@ int convert_csr(Matrix &m, const int64_t *d_row_ptr, const int32_t *d_col_idx,
     a.colidx = m.colidx;
     a.masks = m.masks;
     a.vout = m.values;
+    SPC5_CUDA(cudaEventRecord(ev[2], st));
     launch_convert<true>(m.r, a, st);
     SPC5_CUDA(cudaGetLastError());
     if (m.r == 1)  // slot order == CSR order for single-row panels
         SPC5_CUDA(cudaMemcpyAsync(m.values, d_values, (size_t)m.nnz * m.value_bytes(),
                                   cudaMemcpyDeviceToDevice, st));
+    SPC5_CUDA(cudaEventRecord(ev[3], st));
+    SPC5_CUDA(cudaEventSynchronize(ev[3]));
+    cudaEventElapsedTime(&m.k1_count_ms, ev[0], ev[1]);
+    cudaEventElapsedTime(&m.k1_fill_ms, ev[2], ev[3]);
     note_launches(m.r == 1 ? 2 : 2);
     return SPC5_OK;
 }

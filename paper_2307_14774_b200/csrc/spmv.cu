@@ -1635,6 +1635,50 @@ int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
                                      a.accumulate ? 1 : cdiv(a.num_empty, 256));
     grid = std::min<int64_t>(grid, (int64_t)m.sm_count * per_sm);
     grid = std::max<int64_t>(grid, 1);
+    // SPC5_X_WINDOW=1: an L2 persistence window over x as a launch attribute
+    // (the north star's x-load item).  The set-aside is the
+    // device maximum; a window larger than it persists with hit ratio
+    // set-aside / window.  Off by default: the matrix stream is already
+    // evict-first, and the A/B on configs 2/5 (profiles/SUMMARY_r2.md) shows no gain.
+    static const int x_window = [] {
+        const char *e = getenv("SPC5_X_WINDOW");
+        return e ? atoi(e) : 0;
+    }();
+    if (x_window) {
+        static int max_window = 0, max_persist = 0;
+        static std::once_flag once;
+        std::call_once(once, [] {
+            int dev = 0;
+            cudaGetDevice(&dev);
+            cudaDeviceGetAttribute(&max_window, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+            cudaDeviceGetAttribute(&max_persist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+            if (max_persist > 0) cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, max_persist);
+            if (getenv("SPC5_PLAN_DEBUG"))
+                fprintf(stderr, "spc5 x window: max window %d B, persisting set-aside %d B\n",
+                        max_window, max_persist);
+        });
+        const size_t xb = (size_t)m.num_cols * (m.precision == SPC5_F64 ? 8 : 4);
+        const size_t wb = std::min<size_t>(xb, (size_t)std::max(max_window, 0));
+        if (wb && max_persist > 0) {
+            cudaLaunchAttribute attr[1];
+            attr[0].id = cudaLaunchAttributeAccessPolicyWindow;
+            attr[0].val.accessPolicyWindow.base_ptr = const_cast<void *>(a.x);
+            attr[0].val.accessPolicyWindow.num_bytes = wb;
+            attr[0].val.accessPolicyWindow.hitRatio =
+                (float)std::min(1.0, (double)max_persist / (double)wb);
+            attr[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+            attr[0].val.accessPolicyWindow.missProp = cudaAccessPropertyNormal;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3((unsigned)grid);
+            cfg.blockDim = dim3((unsigned)(wpc * 32));
+            cfg.dynamicSmemBytes = smem;
+            cfg.stream = st;
+            cfg.attrs = attr;
+            cfg.numAttrs = 1;
+            SPC5_CUDA(cudaLaunchKernelEx(&cfg, kernel, a));
+            return SPC5_OK;
+        }
+    }
     kernel<<<(unsigned)grid, wpc * 32, smem, st>>>(a);
     SPC5_CUDA(cudaGetLastError());
     return SPC5_OK;
