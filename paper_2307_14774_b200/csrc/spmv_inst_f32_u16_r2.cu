@@ -1,0 +1,7 @@
+// One K2 instance per translation unit (parallel build): see spmv_kernel.cuh.
+#include "spmv_kernel.cuh"
+namespace spc5 {
+int launch_k2_f32_u16_r2(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
+    return launch_typed<float, uint16_t, 2>(m, a, st);
+}
+}  // namespace spc5

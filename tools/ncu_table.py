@@ -13,7 +13,7 @@ import os
 import sys
 
 SCALE = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "nsecond": 1e-3, "usecond": 1,
-         "msecond": 1e3, "": 1, "%": 1, "inst": 1, "sector": 1, "request": 1, "warp": 1,
+         "msecond": 1e3, "ns": 1e-3, "us": 1, "ms": 1e3, "s": 1e6, "": 1, "%": 1, "inst": 1, "sector": 1, "request": 1, "warp": 1,
          "register/thread": 1}
 
 
