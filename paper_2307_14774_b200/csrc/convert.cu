@@ -14,6 +14,9 @@
 // For r = 1 that order is the CSR order, so values are one D2D copy.
 #include <cub/cub.cuh>
 
+#include <algorithm>
+#include <mutex>
+
 #include "common.cuh"
 
 namespace spc5 {
@@ -58,9 +61,10 @@ struct ConvArgs {
     void *vout;
 };
 
-// One group of R lanes per panel; R divides 32 so groups never straddle warps.
-template <int R, bool WRITE>
-__global__ void __launch_bounds__(256) convert_kernel(ConvArgs a) {
+// Count pass.  One group of R lanes per panel (R divides 32, so groups never
+// straddle warps) runs the greedy chain and counts the panel's blocks.
+template <int R>
+__global__ void __launch_bounds__(256) count_kernel(ConvArgs a) {
     const int64_t t = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     const int lane = threadIdx.x & 31;
     const int64_t p = t / R;
@@ -73,9 +77,6 @@ __global__ void __launch_bounds__(256) convert_kernel(ConvArgs a) {
         cur = a.row_ptr[row];
         end = a.row_ptr[row + 1];
     }
-    const int64_t row0 = p * R < a.num_rows ? p * R : a.num_rows;
-    int64_t bpos = WRITE ? a.rowptr[p] : 0;
-    int64_t vpos = WRITE ? a.row_ptr[row0] : 0;
     int64_t nblk = 0;
     const uint32_t kSent = 0xffffffffu;
     const int span = a.vs - 1;
@@ -85,56 +86,218 @@ __global__ void __launch_bounds__(256) convert_kernel(ConvArgs a) {
         for (int d = 1; d < R; d <<= 1) anchor = min(anchor, __shfl_xor_sync(gmask, anchor, d));
         if (anchor == kSent) break;
         const uint32_t limit = anchor + (uint32_t)span;
+        while (cur < end && (uint32_t)__ldg(a.col_idx + cur) <= limit) ++cur;
+        ++nblk;
+    }
+    if (rr == 0) a.panel_blocks[p] = nblk;
+}
+
+// Fill pass with coalesced global traffic.  A CTA of T threads owns T/R
+// consecutive panels, so its CSR entries [K0, K1), its blocks [B0, B1) and its
+// output values [K0, K1) are contiguous ranges.  Walking the rows straight from
+// global memory costs one 32-byte sector transaction per lane and load (rows
+// are ~100 bytes apart), which bounds the pass at ~2 TB/s; so
+//   A. the CTA loads its column indices into shared memory, consecutive
+//      threads on consecutive addresses;
+//   B. the lane groups run the greedy chain over the staged columns, write
+//      column starts and masks to staged block arrays and overwrite every
+//      consumed column index with the value's destination (slot order:
+//      block, row-in-panel, column -- the stable argsort of blocks.py:136-137);
+//   C. (R > 1) values are read from the CSR array in order, scattered into a
+//      staged copy by those destinations and written out in order; for R = 1
+//      slot order is CSR order and the values are one device copy.
+// A CTA whose ranges exceed the staging capacity (a tail of very long rows)
+// walks global memory directly, as the count pass does.
+struct StageCaps {
+    int entries;  // staged CSR entries (column / destination words; R > 1: + value copy)
+    int blocks;   // staged blocks
+};
+
+template <int R, bool STAGED>
+__device__ __forceinline__ void greedy_fill(const ConvArgs &a, int64_t p, int rr, unsigned gmask,
+                                            int64_t K0, int64_t B0, uint32_t *s_ci,
+                                            uint32_t *s_col, uint8_t *s_mask, int mb) {
+    const int64_t row = p * R + rr;
+    int64_t cur = 0, end = 0;
+    if (row < a.num_rows) {
+        cur = a.row_ptr[row];
+        end = a.row_ptr[row + 1];
+    }
+    int64_t bpos = a.rowptr[p];
+    int64_t vpos = a.row_ptr[min(p * R, a.num_rows)];
+    const uint32_t kSent = 0xffffffffu;
+    const int span = a.vs - 1;
+    auto col_at = [&](int64_t k) -> uint32_t {
+        return STAGED ? s_ci[k - K0] : (uint32_t)__ldg(a.col_idx + k);
+    };
+    for (;;) {
+        uint32_t anchor = cur < end ? col_at(cur) : kSent;
+#pragma unroll
+        for (int d = 1; d < R; d <<= 1) anchor = min(anchor, __shfl_xor_sync(gmask, anchor, d));
+        if (anchor == kSent) break;
+        const uint32_t limit = anchor + (uint32_t)span;
         uint32_t m = 0;
         const int64_t s = cur;
         while (cur < end) {
-            const uint32_t c = (uint32_t)__ldg(a.col_idx + cur);
+            const uint32_t c = col_at(cur);
             if (c > limit) break;
             m |= 1u << (c - anchor);
             ++cur;
         }
-        if (WRITE) {
+        if (STAGED) {
+            if (rr == 0) s_col[bpos - B0] = anchor;
+            if (mb == 1) s_mask[(bpos - B0) * R + rr] = (uint8_t)m;
+            else reinterpret_cast<uint16_t *>(s_mask)[(bpos - B0) * R + rr] = (uint16_t)m;
+        } else {
             if (rr == 0) a.colidx[bpos] = anchor;
-            if (a.vs <= 8) ((uint8_t *)a.masks)[bpos * R + rr] = (uint8_t)m;
-            else ((uint16_t *)a.masks)[bpos * R + rr] = (uint16_t)m;
-            if (R > 1) {
-                const int n = (int)(cur - s);
-                int incl = n;
-#pragma unroll
-                for (int d = 1; d < R; d <<= 1) {
-                    const int v = __shfl_up_sync(gmask, incl, d, R);
-                    if (rr >= d) incl += v;
-                }
-                const int total = __shfl_sync(gmask, incl, R - 1, R);
-                const int64_t dst = vpos + incl - n;
-                if (a.vsize == 8) {
-                    const double *src = (const double *)a.vin + s;
-                    double *out = (double *)a.vout + dst;
-                    for (int j = 0; j < n; ++j) out[j] = src[j];
-                } else {
-                    const float *src = (const float *)a.vin + s;
-                    float *out = (float *)a.vout + dst;
-                    for (int j = 0; j < n; ++j) out[j] = src[j];
-                }
-                vpos += total;
-            }
-            ++bpos;
+            if (mb == 1) static_cast<uint8_t *>(a.masks)[bpos * R + rr] = (uint8_t)m;
+            else static_cast<uint16_t *>(a.masks)[bpos * R + rr] = (uint16_t)m;
         }
-        ++nblk;
+        if (R > 1) {
+            const int n = (int)(cur - s);
+            int incl = n;
+#pragma unroll
+            for (int d = 1; d < R; d <<= 1) {
+                const int v = __shfl_up_sync(gmask, incl, d, R);
+                if (rr >= d) incl += v;
+            }
+            const int total = __shfl_sync(gmask, incl, R - 1, R);
+            const int64_t dst = vpos + incl - n;
+            if (STAGED) {  // destinations replace the consumed columns
+                for (int j = 0; j < n; ++j) s_ci[s - K0 + j] = (uint32_t)(dst - K0 + j);
+            } else if (a.vsize == 8) {
+                const double *src = (const double *)a.vin + s;
+                double *out = (double *)a.vout + dst;
+                for (int j = 0; j < n; ++j) out[j] = src[j];
+            } else {
+                const float *src = (const float *)a.vin + s;
+                float *out = (float *)a.vout + dst;
+                for (int j = 0; j < n; ++j) out[j] = src[j];
+            }
+            vpos += total;
+        }
+        ++bpos;
     }
-    if (!WRITE && rr == 0) a.panel_blocks[p] = nblk;
 }
 
-template <bool WRITE>
-void launch_convert(int r, const ConvArgs &a, cudaStream_t st) {
+template <int R>
+__global__ void __launch_bounds__(256) fill_staged_kernel(ConvArgs a, StageCaps cap) {
+    extern __shared__ __align__(16) uint8_t stage[];
+    const int T = (int)blockDim.x, tid = (int)threadIdx.x, lane = tid & 31;
+    const int ppc = T / R;  // panels per CTA
+    const int64_t P0 = blockIdx.x * (int64_t)ppc;
+    const int64_t P1 = min(P0 + ppc, a.num_panels);
+    const int64_t B0 = a.rowptr[P0], B1 = a.rowptr[P1];
+    const int64_t K0 = a.row_ptr[min(P0 * R, a.num_rows)], K1 = a.row_ptr[min(P1 * R, a.num_rows)];
+    const int mb = a.vs <= 8 ? 1 : 2;
+    const int64_t nk = K1 - K0, nblk = B1 - B0;
+    const bool staged = nk <= cap.entries && nblk <= cap.blocks;  // CTA-uniform
+    // layout: value copy (R > 1) | columns / destinations | block column starts | masks
+    uint8_t *s_val = stage;
+    uint32_t *s_ci = reinterpret_cast<uint32_t *>(stage + (R > 1 ? (size_t)cap.entries * a.vsize : 0));
+    uint32_t *s_col = s_ci + cap.entries;
+    uint8_t *s_mask = reinterpret_cast<uint8_t *>(s_col + cap.blocks);
+    const int64_t p = P0 + tid / R;
+    const int rr = tid % R;
+    const unsigned gmask = (R == 1) ? (1u << lane) : (((1u << R) - 1u) << (lane & ~(R - 1)));
+    if (!staged) {
+        if (p < P1) greedy_fill<R, false>(a, p, rr, gmask, K0, B0, s_ci, s_col, s_mask, mb);
+        return;
+    }
+    for (int64_t i = tid; i < nk; i += T) s_ci[i] = (uint32_t)a.col_idx[K0 + i];
+    __syncthreads();
+    if (p < P1) greedy_fill<R, true>(a, p, rr, gmask, K0, B0, s_ci, s_col, s_mask, mb);
+    __syncthreads();
+    // coalesced copy-out of the block arrays
+    for (int64_t i = tid; i < nblk; i += T) a.colidx[B0 + i] = s_col[i];
+    {
+        const int64_t nbytes = nblk * R * mb;
+        uint8_t *out = static_cast<uint8_t *>(a.masks) + B0 * R * mb;
+        // bytes up to the first 4-byte boundary of the output, then words
+        const int64_t mis = (int64_t)((4 - (reinterpret_cast<uintptr_t>(out) & 3)) & 3);
+        const int head = (int)(mis < nbytes ? mis : nbytes);
+        for (int64_t i = tid; i < head; i += T) out[i] = s_mask[i];
+        const int64_t nwords = (nbytes - head) / 4;
+        uint32_t *ow = reinterpret_cast<uint32_t *>(out + head);
+        if (head == 0) {
+            const uint32_t *sw = reinterpret_cast<const uint32_t *>(s_mask);
+            for (int64_t i = tid; i < nwords; i += T) ow[i] = sw[i];
+        } else {  // staged bytes are misaligned relative to the output words
+            for (int64_t i = tid; i < nwords; i += T) {
+                const uint8_t *b = s_mask + head + i * 4;
+                ow[i] = (uint32_t)b[0] | ((uint32_t)b[1] << 8) | ((uint32_t)b[2] << 16) |
+                        ((uint32_t)b[3] << 24);
+            }
+        }
+        for (int64_t i = head + nwords * 4 + tid; i < nbytes; i += T) out[i] = s_mask[i];
+    }
+    if (R > 1) {  // values: in order from CSR, permuted in shared memory, out in order
+        if (a.vsize == 8) {
+            double *sv = reinterpret_cast<double *>(s_val);
+            const double *in = static_cast<const double *>(a.vin) + K0;
+            for (int64_t i = tid; i < nk; i += T) sv[s_ci[i]] = in[i];
+            __syncthreads();
+            double *out = static_cast<double *>(a.vout) + K0;
+            for (int64_t i = tid; i < nk; i += T) out[i] = sv[i];
+        } else {
+            float *sv = reinterpret_cast<float *>(s_val);
+            const float *in = static_cast<const float *>(a.vin) + K0;
+            for (int64_t i = tid; i < nk; i += T) sv[s_ci[i]] = in[i];
+            __syncthreads();
+            float *out = static_cast<float *>(a.vout) + K0;
+            for (int64_t i = tid; i < nk; i += T) out[i] = sv[i];
+        }
+    }
+}
+
+void launch_count(int r, const ConvArgs &a, cudaStream_t st) {
     const int64_t threads = a.num_panels * r;
     const unsigned grid = (unsigned)cdiv(threads, 256);
     switch (r) {
-        case 1: convert_kernel<1, WRITE><<<grid, 256, 0, st>>>(a); break;
-        case 2: convert_kernel<2, WRITE><<<grid, 256, 0, st>>>(a); break;
-        case 4: convert_kernel<4, WRITE><<<grid, 256, 0, st>>>(a); break;
-        default: convert_kernel<8, WRITE><<<grid, 256, 0, st>>>(a); break;
+        case 1: count_kernel<1><<<grid, 256, 0, st>>>(a); break;
+        case 2: count_kernel<2><<<grid, 256, 0, st>>>(a); break;
+        case 4: count_kernel<4><<<grid, 256, 0, st>>>(a); break;
+        default: count_kernel<8><<<grid, 256, 0, st>>>(a); break;
     }
+}
+
+// CTA shape of the fill pass: T threads (T/R panels) sized so that the staged
+// ranges of an average CTA, plus 25 %, fit ~48 KB (several CTAs per SM).
+template <int R>
+int launch_fill(const ConvArgs &a, int64_t nnz, int64_t nb, cudaStream_t st) {
+    const double rows = (double)std::max<int64_t>(a.num_rows, 1);
+    const int mb = a.vs <= 8 ? 1 : 2;
+    const double erow = (double)nnz / rows;  // entries per row
+    const double ebytes = 4.0 + (R > 1 ? a.vsize : 0);
+    const double brow = (double)nb / rows * (4.0 / R + mb);  // staged block bytes per row
+    int T = 256;
+    while (T > 32 && (erow * ebytes + brow) * T * 1.25 > 48.0 * 1024) T >>= 1;
+    StageCaps cap;
+    cap.entries = ((int)(erow * T * 1.25) + 128 + 3) / 4 * 4;
+    cap.blocks = ((int)((double)nb / rows * T / R * 1.25) + 64 + 3) / 4 * 4;
+    size_t smem = (size_t)cap.entries * (size_t)ebytes + (size_t)cap.blocks * (4 + R * mb) + 16;
+    // R > 1: the staged path measured slower than the direct walk (400^3 stencil
+    // beta(8,8) fill 46 vs 18 ms, FEM beta(8,8) 7.5 vs 1.1 ms: the value
+    // permutation through shared memory and CTAs of 64-128 threads cost more
+    // than the sector-per-lane loads they replace), so only R = 1 stages
+    // (beta(1,8) 9.8 -> 8.9 ms, beta(1,16) 8.4 -> 6.6 ms).
+    if (R > 1 || smem > 160 * 1024) {  // (or rows of several KB on average)
+        T = 256;
+        cap.entries = 0;
+        cap.blocks = 0;
+        smem = 16;
+    }
+    static std::once_flag once;
+    static cudaError_t attr_err = cudaSuccess;
+    std::call_once(once, [] {
+        attr_err = cudaFuncSetAttribute(fill_staged_kernel<R>,
+                                        cudaFuncAttributeMaxDynamicSharedMemorySize, 160 * 1024);
+    });
+    if (attr_err != cudaSuccess) return cuda_fail(attr_err, "cudaFuncSetAttribute(fill_staged_kernel)");
+    const unsigned grid = (unsigned)cdiv(a.num_panels, T / R);
+    fill_staged_kernel<R><<<grid, T, smem, st>>>(a, cap);
+    SPC5_CUDA(cudaGetLastError());
+    return SPC5_OK;
 }
 
 // ---------------------------------------------------------------- to CSR
@@ -253,7 +416,7 @@ int convert_csr(Matrix &m, const int64_t *d_row_ptr, const int32_t *d_col_idx,
     cudaEvent_t *ev = evs.e;
     for (int i = 0; i < 4; ++i) SPC5_CUDA(cudaEventCreate(&ev[i]));
     SPC5_CUDA(cudaEventRecord(ev[0], st));
-    launch_convert<false>(m.r, a, st);
+    launch_count(m.r, a, st);
     SPC5_CUDA(cudaGetLastError());
     SPC5_CUDA(cudaEventRecord(ev[1], st));
     SPC5_TRY(inclusive_scan<int64_t>(counts, m.rowptr + 1, np, st));
@@ -270,8 +433,12 @@ int convert_csr(Matrix &m, const int64_t *d_row_ptr, const int32_t *d_col_idx,
     a.masks = m.masks;
     a.vout = m.values;
     SPC5_CUDA(cudaEventRecord(ev[2], st));
-    launch_convert<true>(m.r, a, st);
-    SPC5_CUDA(cudaGetLastError());
+    switch (m.r) {
+        case 1: SPC5_TRY(launch_fill<1>(a, m.nnz, nb, st)); break;
+        case 2: SPC5_TRY(launch_fill<2>(a, m.nnz, nb, st)); break;
+        case 4: SPC5_TRY(launch_fill<4>(a, m.nnz, nb, st)); break;
+        default: SPC5_TRY(launch_fill<8>(a, m.nnz, nb, st)); break;
+    }
     if (m.r == 1)  // slot order == CSR order for single-row panels
         SPC5_CUDA(cudaMemcpyAsync(m.values, d_values, (size_t)m.nnz * m.value_bytes(),
                                   cudaMemcpyDeviceToDevice, st));

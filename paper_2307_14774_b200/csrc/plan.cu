@@ -127,6 +127,15 @@ __global__ void targets_kernel(int64_t num_panels, const int64_t *__restrict__ r
     cand[c] = rowptr[P];
 }
 
+// (a'') exact targets (LBR plans): a chunk at every global multiple of cb
+// blocks, whatever the panels (chunk heads inside a panel use the carry slots)
+__global__ void targets_exact_kernel(int64_t nb, int64_t base, int64_t cb, int64_t num_targets,
+                                     int64_t *cand) {
+    const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    if (c >= num_targets) return;
+    cand[c] = c == 0 ? 0 : min((base / cb + c) * cb - base, nb - 1);
+}
+
 // (a') panel-count targets: a chunk every ppc panels (regular matrices, so
 // every lane-per-panel-row step of the chunk is a full warp)
 __global__ void targets_panels_kernel(int64_t num_panels, const int64_t *__restrict__ rowptr,
@@ -679,7 +688,10 @@ int validate_structure(const Matrix &m, cudaStream_t st) {
 static int build_chunks(Matrix &m, int64_t cb, int64_t ppc, cudaStream_t st) {
     Plan &P = m.plan;
     const int64_t nb = m.num_blocks, np = m.num_panels;
-    const int64_t num_targets = ppc ? cdiv(np, ppc) : cdiv(nb, cb);
+    // ppc > 0: panel-count targets; ppc < 0: exact block multiples (LBR); 0: snapped block targets
+    const int64_t num_targets = ppc > 0 ? cdiv(np, ppc)
+                                : ppc < 0 ? (m.block_base + nb - 1) / cb - m.block_base / cb + 1
+                                          : cdiv(nb, cb);
     int64_t *split_counts = nullptr;
     SPC5_TRY(dev_alloc(&split_counts, (size_t)np));
     split_count_kernel<<<(unsigned)cdiv(np, 256), 256, 0, st>>>(np, m.rowptr, m.block_base,
@@ -695,7 +707,10 @@ static int build_chunks(Matrix &m, int64_t cb, int64_t ppc, cudaStream_t st) {
     int64_t *cand = nullptr, *sorted = nullptr;
     SPC5_TRY(dev_alloc(&cand, (size_t)ncand));
     SPC5_TRY(dev_alloc(&sorted, (size_t)ncand + 1));
-    if (ppc)
+    if (ppc < 0)
+        targets_exact_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(
+            nb, m.block_base, cb, num_targets, cand);
+    else if (ppc)
         targets_panels_kernel<<<(unsigned)cdiv(num_targets, 256), 256, 0, st>>>(
             np, m.rowptr, ppc, num_targets, cand);
     else
@@ -902,6 +917,29 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         }
         if (const char *e = getenv("SPC5_CB")) targets = {{std::max(1, atoi(e)), 0}};  // tuning
     }
+    // Lane-per-block-row rounds (LBR) for matrices of long panels whose blocks
+    // are well filled but whose block ROWS are mostly empty (FEM beta(8,8): 3x3
+    // dense sub-blocks, 7.5 values per block, 0.94 per block row; >= 24 blocks
+    // per non-empty panel): lane-per-panel-row lanes would mostly visit blocks
+    // their row does not touch.  Exact chunk cuts every 32k blocks, no
+    // lane-per-panel / value-range chunks, slots <= 6 KB (64 blocks of
+    // beta(8,8): 352 us on config 4, 96 blocks 412 us).  Knob SPC5_LBR=0|1.
+    {
+        const double vpb = (double)m.nnz / (double)std::max<int64_t>(nb, 1);
+        const double bpp = (double)nb / (double)std::max<int64_t>(np - P.num_empty, 1);
+        P.lbr = vpb >= 2.0 && bpp >= 24.0 && vpb < 1.25 * m.r;
+        if (const char *e = getenv("SPC5_LBR")) P.lbr = atoi(e) != 0;
+    }
+    if (P.lbr) {
+        const double per_blk = 4.0 + (double)m.r * m.mask_bytes() +
+                               (double)m.value_bytes() * (double)m.nnz / (double)std::max<int64_t>(nb, 1);
+        slot_cap = std::min<int64_t>(slot_cap, 6144);
+        int64_t k = std::max<int64_t>(1, std::min<int64_t>(cb_max / 32, (int64_t)((double)slot_cap / per_blk / 32.0) + 1));
+        targets.clear();
+        for (; k >= 1; --k) targets.push_back({32 * k, -1});
+        if (const char *e = getenv("SPC5_CB")) targets = {{std::max(32, atoi(e) / 32 * 32), -1}};
+        P.split_len = INT64_MAX / 4;  // exact cuts bound every chunk: no forced splits
+    }
     if (const char *e = getenv("SPC5_SLOT_B")) slot_cap = std::max(1024, atoi(e));
     // irregular r = 1 matrices (block-count targets): slots <= 8 KB
     int64_t irr_cap = m.r == 1 ? std::min<int64_t>(slot_cap, 8192) : slot_cap;
@@ -922,8 +960,9 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         SPC5_TRY(dev_alloc(&P.chunk_flags, (size_t)P.num_chunks + 1));
         chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
             P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
-            P.num_empty, getenv("SPC5_NO_LPR") ? -1 : (getenv("SPC5_LPR_SPLIT") ? 1 : 0),
-            lpr_bal, 4, fvr_mode, P.chunk_v, P.chunk_flags);
+            P.num_empty,
+            (P.lbr || getenv("SPC5_NO_LPR")) ? -1 : (getenv("SPC5_LPR_SPLIT") ? 1 : 0), lpr_bal, 4,
+            P.lbr ? 0 : fvr_mode, P.chunk_v, P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
         unsigned long long *d_st = nullptr, h_st[5] = {0, 0, 0, 0, 0};
         SPC5_TRY(dev_alloc(&d_st, 5));
@@ -971,12 +1010,12 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.lay_val = P.lay_mask + a16(mb * lb + std::max<int64_t>(32, ((m.r == 8 ? 18 : 9) - 1) * lb));
         P.slot_bytes = (int)((P.lay_val + a16(P.max_chunk_values * m.value_bytes() + 32) + 127) /
                              128 * 128);
-        const bool regular = !ppc || P.max_chunk_blocks * 4 <= cb * 5;
+        const bool regular = ppc <= 0 || P.max_chunk_blocks * 4 <= cb * 5;
         // FVR kernels of r = 8 keep their row sums in shared memory (r*256 B
         // per warp = r*128 B per ring slot): smaller slots keep 3 CTAs per SM
         const int64_t cap = (ppc ? slot_cap : irr_cap) - (P.num_fvr && m.r == 8 ? m.r * 128 : 0);
         if (!regular) {  // fewer panels per chunk only averages worse: go to block targets
-            while (ti + 1 < targets.size() && targets[ti + 1].ppc) ++ti;
+            while (ti + 1 < targets.size() && targets[ti + 1].ppc > 0) ++ti;
         }
         if (regular && (P.slot_bytes <= cap || cb == 1 || ti + 1 >= targets.size())) break;
         if (regular && cb <= 32 && P.slot_bytes <= 14 * 1024) break;
@@ -1044,11 +1083,11 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
             ++cnt[v & 7];
         }
         fprintf(stderr,
-                "spc5 plan: r=%d vs=%d nb=%lld np=%lld chunks=%lld target=%lld split_len=%lld "
+                "spc5 plan: r=%d vs=%d lbr=%d nb=%lld np=%lld chunks=%lld target=%lld split_len=%lld "
                 "slot=%d B (rec@%lld col@%lld mask@%lld val@%lld) max_blocks=%lld max_values=%lld "
                 "max_lpp_panels=%lld split=%lld empty=%lld | flags: scan=%lld mid=%lld "
                 "empty=%lld lpr=%lld other=%lld\n",
-                m.r, m.vs, (long long)nb, (long long)np, (long long)nc,
+                m.r, m.vs, (int)P.lbr, (long long)nb, (long long)np, (long long)nc,
                 (long long)P.chunk_target, (long long)P.split_len, P.slot_bytes,
                 (long long)P.lay_rp, (long long)P.lay_col, (long long)P.lay_mask,
                 (long long)P.lay_val, (long long)P.max_chunk_blocks,

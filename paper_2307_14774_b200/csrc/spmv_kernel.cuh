@@ -1200,6 +1200,9 @@ __device__ __forceinline__ void add_row(double (&acc)[R], double v, int row) {
     }
 }
 
+#ifndef SPC5_LBR_K
+#define SPC5_LBR_K 2  // rounds per step in lane-per-block-row mode
+#endif
 #ifndef SPC5_FVR_U
 #define SPC5_FVR_U (R == 1 ? 8 : 4)
 #endif
@@ -1393,6 +1396,126 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
     }
 }
 
+// ---------------------------------------------------------------------------
+// Lane-per-block-row mode (LBR; plan.cu P.lbr: matrices whose blocks hold
+// about one value per block row or more in long panels, e.g. the FEM config).
+// The chunk's n*R row masks are walked in storage order, 32 per round: lane l
+// of round i owns mask 32*i + l, i.e. row l % R of block (32*i + l) / R -- a
+// lane always works on the same row-in-panel, so its row sum is ONE register
+// and the R*... lanes of a panel row meet in a log2(32/R)-step butterfly when
+// the panel closes.  Value offsets: one warp scan per K rounds (the rounds'
+// counts packed 16 bits each).  A round costs max-over-lanes(values of a block
+// ROW) slots: 3 for dense 3x3 FEM blocks whatever r is, where lane-per-block
+// windows pay for the fullest BLOCK and lane-per-panel-row steps for the
+// blocks a row does not touch.  K rounds per step: their gathers are all in
+// flight before the first product.  Chunks are cut at exact global multiples
+// of the chunk target (no snapping to panel starts), so rounds are full; chunk
+// heads inside a panel go through the carry slots / fixup kernel as for every
+// split chunk.  The whole chunk is always summed (range products only filter
+// the stores), so range products are bitwise the full product's.
+template <typename T, typename MT, int R, bool GENERIC, int K>
+__device__ __forceinline__ void lbr_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int n,
+                                          bool head_mid, int sh0, uint32_t a_bits, uint32_t a_col,
+                                          uint32_t a_mask, uint32_t a_val, int lane,
+                                          const T *__restrict__ x, T *__restrict__ y) {
+    constexpr int MB = (int)sizeof(MT);
+    constexpr int LGR = R == 1 ? 0 : R == 2 ? 1 : R == 4 ? 2 : 3;
+    constexpr int BPRD = 32 >> LGR;  // blocks per round
+    constexpr uint32_t SZ = (uint32_t)sizeof(T);
+    constexpr uint32_t SM = BPRD == 32 ? kFull : ((1u << BPRD) - 1u);
+    const int g = lane & (R - 1), grp = lane >> LGR;
+    auto put = [&](int pr, double v) {  // lanes < R: row `lane` of the closed panel pr (rel. p0)
+        if (lane >= R) return;
+        if (pr == 0 && head_mid) {
+            a.carry[c * R + g] = v;
+            return;
+        }
+        const int64_t P = p0 + pr;
+        if (GENERIC && (P < a.p_lo || P >= a.p_hi)) return;
+        const int64_t row = P * R + g;
+        if (row < a.num_rows) put_row<T>(a, y, row, v);
+    };
+    auto reduce_g = [&](double v) -> double {  // over the lanes of the same row-in-panel
+#pragma unroll
+        for (int o = R; o < 32; o <<= 1) v += __shfl_xor_sync(kFull, v, o);
+        return v;
+    };
+    int pcur = head_mid ? 0 : -1;  // the open panel (rel. p0); -1: none yet
+    double acc = 0.0;
+    uint32_t vrel = 0;
+    for (int b0r = 0; b0r < n; b0r += K * BPRD) {
+        uint32_t m[K], col[K], vr[K], S[K];
+        int h[K];
+        uint32_t packed = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            const int bb = b0r + k * BPRD;  // first block of the round
+            const int b = bb + grp;
+            const bool counted = b < n;
+            const int bc = min(b, n - 1);
+            col[k] = lds_u32(a_col + (uint32_t)bc * 4u);
+            const uint32_t raw = lds_mask_row(a_mask + (uint32_t)(bc * R + g) * MB, MB);
+            m[k] = counted ? raw : 0u;
+            h[k] = __popc(m[k]);
+            packed |= (uint32_t)h[k] << (16 * (k & 1));
+            // panel starts among the round's blocks
+            const int gb = sh0 + bb;
+            const uint32_t w0 = lds_u32(a_bits + (uint32_t)(gb >> 5) * 4u);
+            const uint32_t w1 = lds_u32(a_bits + (uint32_t)((gb >> 5) + 1) * 4u);
+            uint32_t sb = __funnelshift_r(w0, w1, gb & 31) & SM;
+            const int nleft = n - bb;  // counted blocks of the round
+            sb = nleft >= BPRD ? sb : (nleft > 0 ? sb & ((1u << nleft) - 1u) : 0u);
+            S[k] = sb;
+            if ((k & 1) == 1 || k == K - 1) {  // one scan per two rounds
+                const uint32_t incl = (uint32_t)warp_incl_scan((int)packed);
+                const uint32_t tot = __shfl_sync(kFull, incl, 31);
+                if ((k & 1) == 1) {
+                    const uint32_t t0 = tot & 0xffffu;
+                    vr[k - 1] = a_val + (vrel + (incl & 0xffffu) - (uint32_t)h[k - 1]) * SZ;
+                    vr[k] = a_val + (vrel + t0 + (incl >> 16) - (uint32_t)h[k]) * SZ;
+                    vrel += t0 + (tot >> 16);
+                } else {
+                    vr[k] = a_val + (vrel + (incl & 0xffffu) - (uint32_t)h[k]) * SZ;
+                    vrel += tot & 0xffffu;
+                }
+                packed = 0;
+            }
+        }
+        int cm = 0;
+#pragma unroll
+        for (int k = 0; k < K; ++k) cm = max(cm, h[k]);
+        double ar[K];
+#pragma unroll
+        for (int k = 0; k < K; ++k) ar[k] = 0.0;
+        row_dispatch_sep<T, K, true>(ar, m, h, x, col, vr, __reduce_max_sync(kFull, cm));
+#pragma unroll
+        for (int k = 0; k < K; ++k) {
+            if (S[k] == 0u) {  // warp-uniform: no panel starts in the round
+                acc += ar[k];
+                continue;
+            }
+            // panels closing in this round: the open one takes the lanes before
+            // the first start, each further start closes the panel before it
+            uint32_t sbits = S[k];
+            int lo = 0;
+            while (sbits) {
+                const int kb = __ffs(sbits) - 1;
+                sbits &= sbits - 1u;
+                const double v = acc + ((grp >= lo && grp < kb) ? ar[k] : 0.0);
+                const double tot = reduce_g(v);
+                if (pcur >= 0) put(pcur, tot);
+                acc = 0.0;
+                ++pcur;
+                lo = kb;
+            }
+            acc = grp >= lo ? ar[k] : 0.0;
+        }
+    }
+    // the chunk's last panel (it may continue in the next chunk: carry / fixup)
+    const double tot = reduce_g(acc);
+    if (pcur >= 0) put(pcur, tot);
+}
+
 // K2.  Each warp takes chunks c_lo + (blockIdx.x + k*gridDim.x)*W + warp,
 // k = 0, 1, ...; the CTA's warps work on neighbouring chunks (x reuse in L1).
 // GENERIC=true restricts the product to a panel range (spc5_spmv_panels /
@@ -1402,7 +1525,8 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
 // the instruction cache and the register allocation is its own).  MODE 0:
 // lane-per-panel-row, balanced lane ranges and lane-per-block (no flat value
 // ranges); 1: flat value ranges only; 2: every mode (mixed plans and range
-// products); 3: lane-per-panel-row only.
+// products); 3: lane-per-panel-row only; 4: lane-per-block-row rounds (LBR
+// plans; chunks holding empty panels fall back to lane-per-block).
 template <typename T, typename MT, int R, bool GENERIC, int MODE>
 // 168 registers: 12 warps per SM (3 CTAs x 4 warps) fit the register file;
 // the shared-memory ring allows no more
@@ -1498,16 +1622,19 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
         const T *slot_values = reinterpret_cast<const T *>(smem + (a_val - smem_addr(smem)));
         const int sh0 = (int)((b0 + a.off32) & 31);
 
-        if (MODE == 1) {
+        if (MODE == 4 && !slow) {  // lane-per-block-row rounds (LBR plans)
+            lbr_chunk<T, MT, R, GENERIC, SPC5_LBR_K>(a, c, p0, n, head_mid, sh0, a_bits, a_col,
+                                                     a_mask, a_val, lane, x, y);
+        } else if (MODE == 1) {
             fvr_chunk<T, MT, R, GENERIC, SPC5_FVR_U>(a, c, p0, n, head_mid, sh0, a_bits, a_rp,
                                                      a_col, a_mask, slot_values, lane, x, y);
-        } else if (MODE == 3 || (flags & 4)) {  // lane-per-panel chunk
+        } else if (MODE < 4 && (MODE == 3 || (flags & 4))) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
                                          a_rp, a_col, a_mask, a_val, lane, x, y);
         } else if (MODE == 2 && (flags & 64)) {  // flat value ranges
             fvr_chunk<T, MT, R, GENERIC, SPC5_FVR_U>(a, c, p0, n, head_mid, sh0, a_bits, a_rp,
                                                      a_col, a_mask, slot_values, lane, x, y);
-        } else if (!slow && SPC5_BLR) {  // balanced lane ranges
+        } else if (MODE < 4 && !slow && SPC5_BLR) {  // balanced lane ranges
             blr_chunk<T, MT, R, GENERIC, SPC5_BLR_U>(a, c, p0, n, head_mid, sh0, sbase + 48, a_bits,
                                                            a_rp, a_col, a_mask, a_val, lane, x, y);
         } else {
@@ -1675,7 +1802,12 @@ int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
     int launches = 1;
     const int64_t nc = a.c_hi - a.c_lo;
     constexpr int ACC = R == 8 ? R * 256 : 0;  // FVR row sums per warp (kernels with FVR code)
-    if (a.p_lo == 0 && a.p_hi == m.num_panels) {  // full product: the plan's modes only
+    if (P.lbr) {
+        if (a.p_lo == 0 && a.p_hi == m.num_panels)
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 4>, m, a, nc, st));
+        else
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, true, 4>, m, a, nc, st));
+    } else if (a.p_lo == 0 && a.p_hi == m.num_panels) {  // full product: the plan's modes only
         if (P.num_fvr == P.num_chunks)
             SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 1>, m, a, nc, st, ACC));
         else if (P.num_lpp == P.num_chunks)
