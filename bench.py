@@ -441,10 +441,28 @@ def ours_single(args, formats):
         for f in formats:  # the e2e result is the device result
             assert torch.equal(yp[f].to("cuda"), ys[f]), "e2e result differs from device result"
         del yp
+        # the same call on ordinary (pageable) numpy arrays, as a drop-in caller of
+        # kernels.py:119-129 would pass them: the copies stage through the driver
+        pg_steps = max(2, min(e2e_steps, 5))
+        x_pg = np.array(x_np, copy=True)
+        y_pg = {f: np.empty(num_rows, dtype=x_np.dtype) for f in formats}
+        for f in formats:
+            spmv(mats[f], x_pg, y_pg[f])
+        t0 = time.perf_counter()
+        for _ in range(pg_steps):
+            for f in formats:
+                spmv(mats[f], x_pg, y_pg[f])
+        el_pg = time.perf_counter() - t0
+        for f in formats:
+            assert np.array_equal(y_pg[f], ys[f].cpu().numpy()), "pageable e2e result differs"
+        del y_pg
         e2e = {"value": flops_step * e2e_steps / el / 1e9, "unit": "GFLOP/s",
                "h2d_bytes_per_step": vb * num_cols * len(formats),
                "d2h_bytes_per_step": vb * num_rows * len(formats), "steps": e2e_steps,
-               "path": "paper_2307_14774_b200.spmv(numpy pinned) -> spc5_spmv_host"}
+               "path": "paper_2307_14774_b200.spmv(numpy pinned) -> spc5_spmv_host",
+               "pageable": {"value": flops_step * pg_steps / el_pg / 1e9, "unit": "GFLOP/s",
+                            "steps": pg_steps,
+                            "path": "the same call on pageable numpy arrays"}}
 
     # ---- CPU baseline (oracle port of the reference scalar kernel), rank 0, N=1
     cpu = None

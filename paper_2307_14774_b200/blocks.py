@@ -403,3 +403,61 @@ def load_spc5(path) -> Spc5Matrix:
     off += nb * r * mdt.itemsize
     values = np.frombuffer(raw, vdt, nnz, off).astype(vdt.newbyteorder("="))
     return Spc5Matrix(num_rows, num_cols, r, vs, rowptr, colidx, masks, values)
+
+
+# ---- per-rank shard files -------------------------------------
+# The reference cache (blocks.py:235-272) stores block_rowptr as u4 and knows
+# nothing about shards: the 400^3 matrices have > 2^32 / 8 blocks per format
+# on few ranks and are only ever held as row-panel shards.  Version 2 keeps
+# the reference's array order and little-endian layout, widens block_rowptr to
+# i8 and records where the shard sits in the global matrix.
+_SHARD_VERSION = 2
+_SHARD_HEAD = "<4sIIIqqBxxxqqq" + "qqqii"  # v1 header + global_rows, row_lo, block_base, rank, world
+_IO_CHUNK = 1 << 26  # elements per write/read call (bounded host staging)
+
+
+def save_spc5_shard(s, path, *, global_rows: int, row_lo: int, rank: int, world: int) -> None:
+    """Write rank `rank`'s row-panel shard (rows [row_lo, row_lo + s.num_rows) of a
+    global_rows-row matrix, its blocks numbered from s.block_base)."""
+    s = as_spc5(s)
+    header = struct.pack(_SHARD_HEAD, _MAGIC, _SHARD_VERSION, s.r, s.vs, s.num_rows, s.num_cols,
+                         0 if s.precision == "f32" else 1, s.nnz, s.num_blocks, s.num_panels,
+                         int(global_rows), int(row_lo), int(s.block_base), int(rank), int(world))
+    mdt = "<u1" if s.vs <= 8 else "<u2"
+    vdt = "<f4" if s.precision == "f32" else "<f8"
+    with open(path, "wb") as fh:
+        fh.write(header)
+        for arr, dt in ((s.block_rowptr, "<i8"), (s.block_colidx, "<u4"), (s.block_masks, mdt),
+                        (s.values, vdt)):
+            a = np.asarray(arr)
+            for i in range(0, a.size, _IO_CHUNK):
+                fh.write(a[i:i + _IO_CHUNK].astype(dt, copy=False).tobytes())
+
+
+def load_spc5_shard(path):
+    """Read a shard file: (Spc5Matrix with its block_base, metadata dict)."""
+    hs = struct.calcsize(_SHARD_HEAD)
+    with open(path, "rb") as fh:
+        head = fh.read(hs)
+        if len(head) < hs:
+            raise ValueError("truncated shard file")
+        (magic, version, r, vs, num_rows, num_cols, prec, nnz, nb, npanels, global_rows, row_lo,
+         block_base, rank, world) = struct.unpack(_SHARD_HEAD, head)
+        if magic != _MAGIC:
+            raise ValueError(f"not a block-matrix cache file: bad magic {magic!r}")
+        if version != _SHARD_VERSION:
+            raise ValueError(f"unsupported shard cache version {version}")
+        mdt = np.dtype("<u1") if vs <= 8 else np.dtype("<u2")
+        vdt = np.dtype("<f4") if prec == 0 else np.dtype("<f8")
+
+        def read(dt, count):
+            out = np.fromfile(fh, dtype=dt, count=count)
+            if out.size != count:
+                raise ValueError("truncated shard file")
+            return out
+        rowptr = read(np.dtype("<i8"), npanels + 1)
+        colidx = read(np.dtype("<u4"), nb)
+        masks = read(mdt, nb * r)
+        values = read(vdt, nnz)
+    s = Spc5Matrix(num_rows, num_cols, r, vs, rowptr, colidx, masks, values, block_base=block_base)
+    return s, {"global_rows": global_rows, "row_lo": row_lo, "rank": rank, "world": world}

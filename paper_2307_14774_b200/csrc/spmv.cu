@@ -96,6 +96,12 @@ int launch_spmv(const Matrix &m, int64_t p_lo, int64_t p_hi, const void *x, void
     a.x = x;
     a.y = y;
     a.num_rows = m.num_rows;
+    a.num_cols = m.num_cols;
+#if SPC5_CHECKED
+    // self-test of the checked build: a one-column x bound makes the first
+    // gather past column 0 trap (tools/checked_build.sh expects the failure)
+    if (getenv("SPC5_CHECKED_SELFTEST")) a.num_cols = 1;
+#endif
     a.num_panels = m.num_panels;
     a.chunk_b = P.chunk_b;
     a.chunk_v = P.chunk_v;

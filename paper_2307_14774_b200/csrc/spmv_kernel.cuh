@@ -70,7 +70,7 @@ struct SpmvArgs {
     const void *values;
     const void *x;
     void *y;
-    int64_t num_rows, num_panels;
+    int64_t num_rows, num_cols, num_panels;
     const int64_t *chunk_b, *chunk_v, *chunk_p;
     const uint8_t *chunk_flags;   // bit0 starts inside a panel, bit1 has empty panels
     const uint32_t *pstart_bits;  // panel-start bitmap over 32-block granules
@@ -111,6 +111,43 @@ constexpr uint32_t kRingOff = 512;  // barriers (8 warps x kMaxSlots), records, 
 __device__ __forceinline__ uint32_t smem_addr(const void *p) {
     return (uint32_t)__cvta_generic_to_shared(p);
 }
+// ---- checked build (-DSPC5_CHECKED=1; tools/checked_build.sh) ---------------
+// compute-sanitizer is closed on the GPU pool, so the memcheck part is built
+// in: every shared-memory access of the slot readers must fall inside the
+// CTA's dynamic shared memory, every x gather inside x[0, num_cols) and every
+// y store inside y[0, num_rows); a violation prints where and traps (the
+// launch fails loudly).  Off in the product build: the checks compile away.
+#ifndef SPC5_CHECKED
+#define SPC5_CHECKED 0
+#endif
+#if SPC5_CHECKED
+__shared__ unsigned long long chk_bounds[4];  // x lo/hi, y lo/hi (set by the kernel prologue)
+__device__ __noinline__ void chk_fail(const char *what, unsigned long long v) {
+    printf("SPC5_CHECKED violation: %s at %llx (block %d thread %d)\n", what, v, (int)blockIdx.x,
+           (int)threadIdx.x);
+    __trap();
+}
+__device__ __forceinline__ void chk_smem(uint32_t addr, uint32_t bytes) {
+    extern __shared__ uint8_t chk_dyn[];
+    uint32_t total;
+    asm("mov.u32 %0, %%dynamic_smem_size;" : "=r"(total));
+    const uint32_t base = smem_addr(chk_dyn);
+    if (addr < base || addr + bytes > base + total) chk_fail("shared-memory access", addr);
+}
+__device__ __forceinline__ void chk_x(const void *p, uint32_t bytes) {
+    const unsigned long long v = (unsigned long long)p;
+    if (v < chk_bounds[0] || v + bytes > chk_bounds[1]) chk_fail("x gather", v);
+}
+__device__ __forceinline__ void chk_y(const void *p, uint32_t bytes) {
+    const unsigned long long v = (unsigned long long)p;
+    if (v < chk_bounds[2] || v + bytes > chk_bounds[3]) chk_fail("y store", v);
+}
+#else
+__device__ __forceinline__ void chk_smem(uint32_t, uint32_t) {}
+__device__ __forceinline__ void chk_x(const void *, uint32_t) {}
+__device__ __forceinline__ void chk_y(const void *, uint32_t) {}
+#endif
+
 __device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_addr(bar)), "r"(count)
                  : "memory");
@@ -147,6 +184,7 @@ __device__ __forceinline__ uint64_t evict_first_policy() {
 }
 
 __device__ __forceinline__ uint32_t lds_u32(uint32_t addr) {
+    chk_smem(addr, 4);
     uint32_t v;
     asm volatile("ld.shared.u32 %0, [%1];" : "=r"(v) : "r"(addr));
     return v;
@@ -158,6 +196,7 @@ struct LaneMasks {
     static constexpr int N = (BYTES + 3) / 4;
     uint32_t w[N];
     __device__ __forceinline__ void load(uint32_t addr) {
+        chk_smem(addr, BYTES);
         if constexpr (BYTES == 1) {
             asm volatile("ld.shared.u8 %0, [%1];" : "=r"(w[0]) : "r"(addr));
         } else if constexpr (BYTES == 2) {
@@ -202,6 +241,7 @@ __device__ __forceinline__ uint64_t x_policy() {
 }
 #endif
 __device__ __forceinline__ double ldg_pred(const double *p, bool pred) {
+    if (pred) chk_x(p, 8);
     double v = 0.0;
 #ifdef SPC5_X_PROBE_L1  // timing probe only (wrong results): gathers folded into a few 4 KB windows (L1 hits)
     p = reinterpret_cast<const double *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)0x1fff000);
@@ -218,6 +258,7 @@ __device__ __forceinline__ double ldg_pred(const double *p, bool pred) {
     return v;
 }
 __device__ __forceinline__ float ldg_pred(const float *p, bool pred) {
+    if (pred) chk_x(p, 4);
     float v = 0.0f;
 #ifdef SPC5_X_PROBE_L1
     p = reinterpret_cast<const float *>(reinterpret_cast<uintptr_t>(p) & ~(uintptr_t)0x1fff000);
@@ -237,6 +278,7 @@ template <typename T>
 __device__ __forceinline__ T lds_pred(uint32_t addr, bool pred);
 template <>
 __device__ __forceinline__ double lds_pred<double>(uint32_t addr, bool pred) {
+    if (pred) chk_smem(addr, 8);
     double v = 0.0;
     asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f64 %0, [%1];\n}"
                  : "+d"(v)
@@ -245,6 +287,7 @@ __device__ __forceinline__ double lds_pred<double>(uint32_t addr, bool pred) {
 }
 template <>
 __device__ __forceinline__ float lds_pred<float>(uint32_t addr, bool pred) {
+    if (pred) chk_smem(addr, 4);
     float v = 0.0f;
     asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.f32 %0, [%1];\n}"
                  : "+f"(v)
@@ -317,6 +360,7 @@ __device__ __forceinline__ int warp_incl_scan(int v) {
 // one y row: y[row] (+)= v, mirrored to the peer buffers of the fused exchange
 template <typename T>
 __device__ __forceinline__ void put_row(const SpmvArgs &a, T *y, int64_t row, double v) {
+    chk_y(y + row, (uint32_t)sizeof(T));
     if (a.plain) {  // y = A.x, no mirrors: one store (a uniform branch, not predication)
         y[row] = (T)v;
         return;
@@ -538,6 +582,7 @@ __device__ __forceinline__ void ir_load(const SpmvArgs &a, int64_t c, bool valid
 }
 
 __device__ __forceinline__ int64_t lds_s64(uint32_t addr) {
+    chk_smem(addr, 8);
     int64_t v;
     asm volatile("ld.shared.s64 %0, [%1];" : "=l"(v) : "r"(addr));
     return v;
@@ -622,6 +667,7 @@ __device__ __forceinline__ void pair_slots(double &acc, const uint32_t (&m)[2 * 
 }
 
 __device__ __forceinline__ uint32_t lds_mask_row(uint32_t addr, int mb) {
+    chk_smem(addr, (uint32_t)mb);
     uint32_t v;
     if (mb == 1) asm volatile("ld.shared.u8 %0, [%1];" : "=r"(v) : "r"(addr));
     else asm volatile("ld.shared.u16 %0, [%1];" : "=r"(v) : "r"(addr));
@@ -1112,6 +1158,7 @@ __device__ __forceinline__ void blr_chunk(const SpmvArgs &a, int64_t c, int64_t 
 
 // shared-memory load that only happens when p (else `old` is kept)
 __device__ __forceinline__ uint32_t lds_u32_if(uint32_t addr, bool p, uint32_t old) {
+    if (p) chk_smem(addr, 4);
     uint32_t v = old;
     asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u32 %0, [%1];\n}"
                  : "+r"(v)
@@ -1125,6 +1172,7 @@ struct BlockBits {  // the R masks of one block, row-major, as one bit string of
     uint32_t w[W];
     // (re)load when p
     __device__ __forceinline__ void load_if(uint32_t addr, bool p) {
+        if (p) chk_smem(addr, LB);
         const int q = (int)p;
         if constexpr (LB == 1) {
             asm volatile("{\n .reg .pred q;\n setp.ne.b32 q, %2, 0;\n @q ld.shared.u8 %0, [%1];\n}"
@@ -1309,6 +1357,8 @@ __device__ __forceinline__ void fvr_chunk(const SpmvArgs &a, int64_t c, int64_t 
             xv[u] = T(0);
             vv[u] = T(0);
             if (valid) {
+                chk_x(x + (col + (uint32_t)(pos % BPR)), (uint32_t)sizeof(T));
+                chk_smem(smem_addr(vp + u), (uint32_t)sizeof(T));
                 xv[u] = __ldg(x + (col + (uint32_t)(pos % BPR)));
                 vv[u] = vp[u];
             }
@@ -1546,6 +1596,16 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
     const T *__restrict__ x = static_cast<const T *>(a.x);
     T *__restrict__ y = static_cast<T *>(a.y);
 
+#if SPC5_CHECKED
+    if (threadIdx.x == 0) {
+        chk_bounds[0] = (unsigned long long)a.x;
+        // (a shard reads x up to the matrix's last column: num_cols of the handle)
+        chk_bounds[1] = (unsigned long long)a.x + (unsigned long long)a.num_cols * sizeof(T);
+        chk_bounds[2] = (unsigned long long)a.y;
+        chk_bounds[3] = (unsigned long long)a.y + (unsigned long long)a.num_rows * sizeof(T);
+    }
+    __syncthreads();
+#endif
     const int S = a.nslot;
     uint64_t *bars = reinterpret_cast<uint64_t *>(smem) + warp * kMaxSlots;
     const uint32_t ring = smem_addr(smem) + kRingOff + (uint32_t)(warp * S) * a.lay_bytes;
@@ -1722,8 +1782,9 @@ int launch_ring_kernel(K kernel, const Matrix &m, SpmvArgs a, int64_t nslots,
         const auto key = std::make_tuple((const void *)kernel, wpc, smem);
         auto it = cache.find(key);
         if (it == cache.end()) {
+            // (the checked build's static bounds words count against the 227 KB)
             SPC5_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                           227 * 1024));
+                                           227 * 1024 - (SPC5_CHECKED ? 1024 : 0)));
             // SPC5_CARVEOUT: ask for no more shared memory than the ring of the
             // resident CTAs needs, so the rest stays L1 for the x gathers
             if (getenv("SPC5_CARVEOUT")) {

@@ -28,7 +28,7 @@ from . import _native as nat
 from .blocks import Spc5Matrix, as_spc5, csr_to_spc5, torch_stream
 from .mmio import DTYPES
 
-__all__ = ["KernelConfig", "SpmvResult", "VerifyReport", "spmv", "spmv_spc5_scalar",
+__all__ = ["KernelConfig", "SpmvResult", "VerifyReport", "spmv", "spmv_csr", "spmv_spc5_scalar",
            "spmv_spc5_vector", "csr_reference", "verify_against_oracle",
            "block_value_offsets", "mask_popcounts", "VERIFY_FACTOR"]
 
@@ -127,6 +127,17 @@ def _run(s: Spc5Matrix, x, y, accumulate: bool) -> None:
         y[:s.num_rows] += tmp
     else:
         y[:s.num_rows] = tmp
+
+
+def spmv_csr(m, x, y) -> None:
+    """y[i] += row_i . x for a CsrMatrix (kernels.py:106-118, the reference's CSR
+    comparison kernel).  On the GPU a CSR row is a beta(1, c) panel: the matrix
+    goes through K1 into beta(1, 8|16) and the product through K2, so the sums
+    agree with the sequential loop within the package tolerance."""
+    _check_xy(m.num_rows, m.num_cols, x, y)
+    from .blocks import csr_to_spc5
+    s = csr_to_spc5(m, 1, 8 if m.values.dtype == np.float64 else 16)
+    _run(s, x, y, accumulate=True)
 
 
 def spmv_spc5_scalar(m, x, y) -> None:

@@ -178,3 +178,77 @@ def test_csr_type_duck(spc5):
     m = small_case("hand")
     s = spc5.csr_to_spc5(Csr(m.num_rows, m.num_cols, m.row_ptr, m.col_idx, m.values), 2, 4)
     assert s.block_colidx.tolist() == [0, 6, 6]
+
+
+def test_spmv_csr_matches_sequential_rows(spc5):
+    """spmv_csr (kernels.py:106-118): y[i] += row_i . x, within the package
+    tolerance of the oracle's sequential CSR sums, for both precisions."""
+    from golden_io import case_x, small_case
+    from oracle import oracle
+    from test_gpu_parity import assert_close
+    for name in ("hand", "rand05", "longrows", "longrows_f32", "tall"):
+        m = small_case(name)
+        x = case_x(name, m)
+        y = np.zeros(m.num_rows, m.values.dtype)
+        spc5.spmv_csr(m, x, y)
+        y_ref = np.zeros(m.num_rows, m.values.dtype)
+        oracle.spmv_spc5_scalar(oracle.csr_to_spc5(m, 1, 8), x, y_ref)  # r = 1: CSR row order
+        assert_close(m, y, y_ref, x, f"spmv_csr {name}")
+        again = y.copy()
+        spc5.spmv_csr(m, x, again)  # accumulates
+        assert np.allclose(again, 2 * y, rtol=1e-5 if m.values.dtype == np.float32 else 1e-12, atol=0)
+    with pytest.raises(ValueError):
+        spc5.spmv_csr(small_case("hand"), np.zeros(1), np.zeros(10))
+
+
+def test_shard_cache_files_roundtrip(spc5, tmp_path):
+    """Per-rank shard files: each rank's converted rows written
+    with i8 row pointers and shard metadata, read back bit for bit, and the
+    reloaded shards' products equal the live shards' bit for bit."""
+    from paper_2307_14774_b200.workloads import stencil27_rows, x_vector
+    from paper_2307_14774_b200.distributed import shard_layout
+    n = 16
+    full = stencil27_rows(n, 0, n ** 3)
+    x = x_vector(full.num_cols)
+    for prec_rows, r, vs in ((full, 2, 8), (full, 8, 8)):
+        world = 3
+        layout = shard_layout(full.row_ptr, r, world)
+        whole = spc5.csr_to_spc5(full, r, vs)
+        for rank in range(world):
+            lo, hi = layout.rows(rank)
+            base = int(whole.block_rowptr[layout.panel_ranges[rank][0]])
+            sh = spc5.csr_to_spc5(stencil27_rows(n, lo, hi), r, vs, block_base=base)
+            path = tmp_path / f"shard_{r}_{rank}.spc5"
+            spc5.save_spc5_shard(sh, path, global_rows=n ** 3, row_lo=lo, rank=rank, world=world)
+            back, meta = spc5.load_spc5_shard(path)
+            assert meta == {"global_rows": n ** 3, "row_lo": lo, "rank": rank, "world": world}
+            assert back.block_base == base and back.block_rowptr.dtype == np.int64
+            for f in ("block_rowptr", "block_colidx", "block_masks", "values"):
+                assert np.asarray(getattr(back, f)).tobytes() == np.asarray(getattr(sh, f)).tobytes(), f
+            assert spc5.spmv(back, x).tobytes() == spc5.spmv(sh, x).tobytes()
+    bad = tmp_path / "bad.spc5"
+    bad.write_bytes(b"XXXX" + bytes(100))
+    with pytest.raises(ValueError):
+        spc5.load_spc5_shard(bad)
+
+
+def test_cli_bench_device_cuda(spc5, tmp_path, capsys):
+    """`python -m paper_2307_14774_b200 bench --device cuda` (cli.py:155-185 on the
+    GPU): one line and one CSV v1 record per (format, config), readable by
+    read_records, plus the roofline companion; a non-cuda device is refused."""
+    from paper_2307_14774_b200.__main__ import main
+    out = tmp_path / "bench.csv"
+    rc = main(["bench", "--device", "cuda", "--matrix", "random:600,700,12,0.5,3", "--format",
+               "b1,b4", "--strategy", "scalar,expand", "--reps", "3", "--warmup", "1", "--out",
+               str(out)])
+    assert rc == 0
+    lines = [ln for ln in capsys.readouterr().out.splitlines() if ln.startswith("random:")]
+    assert len(lines) == 4 and all("roofline=" in ln for ln in lines)
+    recs = spc5.read_records(out)
+    assert [(q.r, q.strategy) for q in recs] == [(1, "scalar"), (1, "expand"), (4, "scalar"), (4, "expand")]
+    assert all(q.gflops > 0 and q.matrix == "random:600,700,12,0.5,3" for q in recs)
+    assert (tmp_path / "bench.scatter.csv").exists() and (tmp_path / "bench.gpu.csv").exists()
+    rc = main(["bench", "--device", "cuda", "--matrix", "config:2:0-4096", "--format", "b2",
+               "--reps", "2", "--warmup", "1"])
+    assert rc == 0
+    assert main(["bench", "--device", "cpu", "--matrix", "dense:8"]) == 2

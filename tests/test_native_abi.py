@@ -43,8 +43,54 @@ def test_reference_names_present():
                  "KernelConfig", "SpmvResult", "VerifyReport", "spmv_spc5_scalar",
                  "spmv_spc5_vector", "verify_against_oracle", "Partition", "partition_by_nnz",
                  "spmv_parallel", "run_kernel", "run_bench", "BenchRecord", "CsrMatrix",
-                 "make_random", "make_dense", "make_identity", "spmv"):
+                 "make_random", "make_dense", "make_identity", "spmv", "spmv_csr"):
         assert hasattr(spc5, name), name
+
+
+REFERENCE_SRC = Path("/root/reference/pkg/src")
+
+
+@pytest.mark.skipif(not REFERENCE_SRC.exists(), reason="reference sources only exist in the build container")
+def test_signatures_match_the_reference():
+    """Every hot-path callable the reference exports (spc5/__init__.py:11-21)
+    has the same parameter names, order and defaults here, so its callers
+    (bench.py:153-184 run_bench, cli.py:81-185, its tests) bind unchanged.
+    Extra trailing keyword parameters with defaults are allowed."""
+    import importlib
+    import inspect
+    import sys
+    import paper_2307_14774_b200 as ours
+    sys.path.insert(0, str(REFERENCE_SRC))
+    try:
+        ref = importlib.import_module("spc5")
+    finally:
+        sys.path.remove(str(REFERENCE_SRC))
+    scoped_out = {"CooMatrix", "MatrixSource", "coo_to_csr", "fetch_suitesparse",
+                  "load_matrix_market", "parse_matrix_market"}  # SURVEY 8: parser / fetch
+    checked = 0
+    for name in ref.__all__:
+        if name in scoped_out:
+            continue
+        assert hasattr(ours, name), name
+        r, o = getattr(ref, name), getattr(ours, name)
+        if inspect.isclass(r):
+            if hasattr(r, "__dataclass_fields__"):
+                rf = list(r.__dataclass_fields__)
+                of = list(o.__dataclass_fields__) if hasattr(o, "__dataclass_fields__") else \
+                    list(inspect.signature(o).parameters)
+                assert of[:len(rf)] == rf, (name, rf, of)
+            continue
+        rp = list(inspect.signature(r).parameters.values())
+        op = list(inspect.signature(o).parameters.values())
+        assert [q.name for q in op[:len(rp)]] == [q.name for q in rp], (name, rp, op)
+        for a, b in zip(rp, op):
+            assert (a.default is inspect.Parameter.empty) == (b.default is inspect.Parameter.empty), (name, a.name)
+            if a.default is not inspect.Parameter.empty and not callable(a.default):
+                assert a.default == b.default, (name, a.name, a.default, b.default)
+        for extra in op[len(rp):]:
+            assert extra.default is not inspect.Parameter.empty, (name, extra.name)
+        checked += 1
+    assert checked >= 20
 
 
 def test_kernel_config_validation():
