@@ -505,6 +505,9 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--iters", type=int, default=100,
                     help="N > 1: products of the iterated (all-gather) form per format")
+    ap.add_argument("--fused", action="store_true",
+                    help="N > 1: also time the exchange fused into K2 (NVLink peer stores); "
+                         "off by default at N > 1 because it has only run on one-rank groups")
     ap.add_argument("--scaling", choices=["weak", "strong"], default="strong",
                     help="N > 1: strong = the config's one matrix split over the GPUs "
                          "(default); weak = one n^3 stencil cube of rows per GPU")

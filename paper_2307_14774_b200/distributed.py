@@ -369,6 +369,10 @@ def bench_distributed(args, formats) -> None:
         same_b = bool(torch.equal(xr, xb))
         # the same iterations with the exchange fused into K2 (NVLink stores)
         try:
+            if world > 1 and not (getattr(args, "fused", False) or os.environ.get("SPC5_BENCH_FUSED")):
+                # never run on more than one rank in this environment (one GPU per call):
+                # a hang here would lose the whole line, so it is opt-in (--fused)
+                raise RuntimeError("skipped at N > 1 (pass --fused)")
             ex = FusedExchange(C, tdt, layout, rank)
             ex.run(h, x0, 2, 1.0 / 64.0)
             ft, xf = _timed(lambda: ex.run(h, x0, iters, 1.0 / 64.0).clone(), stream)

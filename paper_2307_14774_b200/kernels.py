@@ -1,17 +1,20 @@
 """SpMV entry points of the reference ``spc5.kernels`` module, run on the GPU.
 
 ``spmv_spc5_scalar`` / ``spmv_spc5_vector`` (kernels.py:205-230) keep their
-signatures, checks and exceptions; both launch K2 (csrc/spmv.cu).  The
+signatures, checks and exceptions; both launch K2 (csrc/spmv_kernel.cuh).  The
 strategy / reduction / x_load toggles of :class:`KernelConfig` select CPU SIMD
 idioms (expand vs compact, hsum vs multi-reduce) that have no counterpart on a
 GPU warp; they are validated and recorded, and only ``precision`` changes what
 runs (kernels.py:47-72, 219-223).
 
-Numerics: products are formed in the matrix precision as in the reference,
-accumulated in fp64 per row (for f32 matrices too) and reduced in a fixed
-order, so results are deterministic run to run and across ``spmv_parallel``
-worker counts; they differ from the reference's strictly sequential order by
-rounding only (tolerance: |dy_i| <= 1e-12 (f64) / 1e-5 (f32) * sum_j |a_ij x_j|).
+Numerics: products are formed in the matrix precision as in the reference and
+row sums are kept in fp64; for f32 matrices in lane-per-panel-row chunks the
+few products of one slot call (<= 27) are first summed with f32 FMAs and that
+partial is added to the fp64 row sum.  Every sum is
+reduced in an order fixed by the plan, so results are deterministic run to run
+and across ``spmv_parallel`` worker counts; they differ from the reference's
+strictly sequential order by rounding only (tolerance: |dy_i| <= 1e-12 (f64) /
+1e-5 (f32) * sum_j |a_ij x_j|).
 
 x / y may be numpy arrays (copied through the host-buffer C entry point) or
 torch CUDA tensors (used in place, on torch's current stream).
