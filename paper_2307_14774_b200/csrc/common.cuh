@@ -41,6 +41,7 @@ struct Plan {
     int64_t num_fvr = 0;            // flat value-range chunks (kernel variant choice)
     int64_t num_lpp = 0;            // lane-per-panel-row chunks
     bool lbr = false;               // lane-per-block-row rounds over exact chunk cuts (plan.cu)
+    bool runs = false;              // every row mask is one contiguous run of bits (K2 RUN gathers)
     int64_t lay_rp = 0, lay_col = 0, lay_mask = 0, lay_val = 0;  // slot: hdr|bits|rec|col|mask|val
     int slot_bytes = 0;
     int64_t num_granules = 0;

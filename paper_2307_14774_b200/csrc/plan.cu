@@ -232,6 +232,20 @@ __global__ void chunk_stats_kernel(int64_t nc, const int64_t *__restrict__ chunk
     atomicMax(out + 1, (unsigned long long)(chunk_v[c + 1] - chunk_v[c]));
 }
 
+// is every row mask one contiguous run of bits (or empty)?  Stencils, bands and
+// dense sub-blocks are; K2's lane-per-panel-row steps then gather x at
+// immediate offsets from the run's top (spmv_kernel.cuh row_slots RUN)
+__global__ void runs_kernel(int64_t nmasks, int vs, const void *__restrict__ masks, int *not_runs) {
+    int bad = 0;
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < nmasks;
+         i += (int64_t)gridDim.x * blockDim.x) {
+        const uint32_t m = load_mask(masks, i, vs);
+        const uint32_t t = m >> (__ffs(m | 0x80000000u) - 1);  // run shifted down to bit 0
+        bad |= (m != 0u && (t & (t + 1u)) != 0u) ? 1 : 0;
+    }
+    if (__any_sync(0xffffffffu, bad) && (threadIdx.x & 31) == 0) atomicOr(not_runs, 1);
+}
+
 // panel-start bitmap over granules (derived plan data, 1 bit per block)
 __global__ void pstart_bits_kernel(int64_t np, const int64_t *__restrict__ rowptr, int off32,
                                    uint32_t *bits) {
@@ -1025,6 +1039,20 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     }
     if (P.slot_bytes > 14 * 1024)
         return fail(SPC5_EINVAL, "a chunk of this matrix does not fit the shared-memory ring");
+    // run plans (knob SPC5_NO_RUN=1 keeps the general bit walk)
+    P.runs = false;
+    if (P.num_lpp == P.num_chunks && !getenv("SPC5_NO_RUN")) {
+        int *d_bad = nullptr, h_bad = 0;
+        SPC5_TRY(dev_alloc(&d_bad, 1));
+        SPC5_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+        runs_kernel<<<(unsigned)std::min<int64_t>(cdiv(nb * m.r, 1024), 148 * 16), 256, 0, st>>>(
+            nb * m.r, m.vs, m.masks, d_bad);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(d_bad);
+        P.runs = h_bad == 0;
+    }
     // panel-start bitmap
     const int off32 = (int)(((m.block_base % 32) + 32) % 32);
     const int64_t ng = cdiv(nb + off32, 32);
@@ -1083,11 +1111,11 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
             ++cnt[v & 7];
         }
         fprintf(stderr,
-                "spc5 plan: r=%d vs=%d lbr=%d nb=%lld np=%lld chunks=%lld target=%lld split_len=%lld "
+                "spc5 plan: r=%d vs=%d lbr=%d runs=%d nb=%lld np=%lld chunks=%lld target=%lld split_len=%lld "
                 "slot=%d B (rec@%lld col@%lld mask@%lld val@%lld) max_blocks=%lld max_values=%lld "
                 "max_lpp_panels=%lld split=%lld empty=%lld | flags: scan=%lld mid=%lld "
                 "empty=%lld lpr=%lld other=%lld\n",
-                m.r, m.vs, (int)P.lbr, (long long)nb, (long long)np, (long long)nc,
+                m.r, m.vs, (int)P.lbr, (int)P.runs, (long long)nb, (long long)np, (long long)nc,
                 (long long)P.chunk_target, (long long)P.split_len, P.slot_bytes,
                 (long long)P.lay_rp, (long long)P.lay_col, (long long)P.lay_mask,
                 (long long)P.lay_val, (long long)P.max_chunk_blocks,

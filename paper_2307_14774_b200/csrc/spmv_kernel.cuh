@@ -403,7 +403,13 @@ __device__ __forceinline__ bool ueq(int v, int k) {
 // highest first.  All U*NS gathers are issued before the first FMA; products
 // are accumulated block by block (storage order).  Slots past a block's count
 // load nothing and add exact zeros.
-template <typename T, int U, int NS>
+// RUN (plans whose every row mask is one contiguous run of bits -- stencils,
+// bands, dense sub-blocks; plan.cu runs_kernel): the columns of a block row are
+// consecutive, so slot u gathers x[top - u] at an immediate offset from the
+// address of the row's highest bit: 2 instructions per slot (predicate, load)
+// instead of 7 (find bit, clear it, column, address, predicate, load).  Same
+// products in the same order as the general walk: bitwise the same sums.
+template <typename T, int U, int NS, bool RUN = false>
 __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h)[U],
                                           const T *__restrict__ x, const uint32_t (&col)[U],
                                           const uint32_t (&vaddr)[U]) {
@@ -417,13 +423,29 @@ __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h
         h[k] = max(h[k] - NS, 0);
     }
     // all x gathers first (the long-latency loads), then values and products
-#pragma unroll
-    for (int u = 0; u < NS; ++u) {
+    if constexpr (RUN) {
+        const T *top[U];
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             const uint32_t pos = bfind(m[k]);
-            m[k] &= ~(1u << pos);
-            xv[k][u] = ldg_pred(x + (col[k] + pos), u < h0[k]);
+            top[k] = x + (col[k] + pos);
+            // the run's top NS bits are consumed (only dense rows come back for more)
+            m[k] = pos + 1u >= (uint32_t)NS ? (m[k] & ((1u << (pos + 1u - NS)) - 1u)) : 0u;
+        }
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+#pragma unroll
+            for (int k = 0; k < U; ++k) xv[k][u] = ldg_pred(top[k] - u, u < h0[k]);
+        }
+    } else {
+#pragma unroll
+        for (int u = 0; u < NS; ++u) {
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const uint32_t pos = bfind(m[k]);
+                m[k] &= ~(1u << pos);
+                xv[k][u] = ldg_pred(x + (col[k] + pos), u < h0[k]);
+            }
         }
     }
     SlotSum<T> sum(acc);
@@ -440,26 +462,27 @@ __device__ __forceinline__ void row_slots(double &acc, uint32_t (&m)[U], int (&h
 
 // One panel row of U blocks with a warp-uniform slot count: the smallest
 // unrolled variant that covers every lane, or batches of 4.
-template <typename T, int U>
+template <typename T, int U, bool RUN = false>
 __device__ __forceinline__ void row_dispatch(double &acc, uint32_t (&m)[U], int (&h)[U],
                                              const T *__restrict__ x, const uint32_t (&col)[U],
                                              const uint32_t (&vaddr)[U], int cmax) {
     if (cmax <= 0) return;
     if (ueq(cmax, 1)) {
-        row_slots<T, U, 1>(acc, m, h, x, col, vaddr);
+        row_slots<T, U, 1, RUN>(acc, m, h, x, col, vaddr);
     } else if (ueq(cmax, 2)) {
-        row_slots<T, U, 2>(acc, m, h, x, col, vaddr);
+        row_slots<T, U, 2, RUN>(acc, m, h, x, col, vaddr);
     } else if (ueq(cmax, 3)) {
-        row_slots<T, U, 3>(acc, m, h, x, col, vaddr);
+        row_slots<T, U, 3, RUN>(acc, m, h, x, col, vaddr);
     } else if (ueq(cmax, 4)) {
-        row_slots<T, U, 4>(acc, m, h, x, col, vaddr);
+        row_slots<T, U, 4, RUN>(acc, m, h, x, col, vaddr);
     } else {  // dense rows: one block at a time so the products stay in order
 #pragma unroll
         for (int k = 0; k < U; ++k) {
             uint32_t mk1[1] = {m[k]};
             int hk1[1] = {h[k]};
             const uint32_t ck1[1] = {col[k]}, vk1[1] = {vaddr[k]};
-            for (int done = 0; done < cmax; done += 4) row_slots<T, 1, 4>(acc, mk1, hk1, x, ck1, vk1);
+            for (int done = 0; done < cmax; done += 4)
+                row_slots<T, 1, 4, RUN>(acc, mk1, hk1, x, ck1, vk1);
         }
     }
 }
@@ -684,7 +707,7 @@ __device__ __forceinline__ uint32_t lds_mask_row(uint32_t addr, int mb) {
 // popcounts the other rows' masks.  Field widths: FB=8 (vs<=8: h<=8, sums
 // over 8 rows <= 64, prefix of 3 totals + rows below <= 248) or FB=16.
 // PAIRS (U even): steps whose pair slots beat block slots use pair_slots.
-template <typename T, typename MT, int R, int U, bool PAIRS>
+template <typename T, typename MT, int R, int U, bool PAIRS, bool RUN = false>
 __device__ __forceinline__ void lpp_steps2(double &acc, int maxlen, int my, int s, int rr, int lg,
                                            int lane, uint32_t vaddr, uint32_t a_col,
                                            uint32_t a_mask, const T *__restrict__ x) {
@@ -760,7 +783,7 @@ __device__ __forceinline__ void lpp_steps2(double &acc, int maxlen, int my, int 
                 mm[k] = m[k];
                 hh[k] = h[k];
             }
-            row_dispatch<T, U>(acc, mm, hh, x, col, vr, cmax);
+            row_dispatch<T, U, RUN>(acc, mm, hh, x, col, vr, cmax);
         } else {  // two halves (register budget of the gathers in flight)
             constexpr int U1 = U / 2, U2 = U - U / 2;
             uint32_t m1[U1], c1[U1], v1[U1], m2[U2], c2[U2], v2[U2];
@@ -775,13 +798,13 @@ __device__ __forceinline__ void lpp_steps2(double &acc, int maxlen, int my, int 
                 m2[k] = m[U1 + k]; c2[k] = col[U1 + k]; v2[k] = vr[U1 + k]; h2[k] = h[U1 + k];
                 cm2 = max(cm2, h[U1 + k]);
             }
-            row_dispatch<T, U1>(acc, m1, h1, x, c1, v1, __reduce_max_sync(kFull, cm1));
-            row_dispatch<T, U2>(acc, m2, h2, x, c2, v2, __reduce_max_sync(kFull, cm2));
+            row_dispatch<T, U1, RUN>(acc, m1, h1, x, c1, v1, __reduce_max_sync(kFull, cm1));
+            row_dispatch<T, U2, RUN>(acc, m2, h2, x, c2, v2, __reduce_max_sync(kFull, cm2));
         }
     }
 }
 
-template <typename T, typename MT, int R, bool GENERIC>
+template <typename T, typename MT, int R, bool GENERIC, bool RUN = false>
 __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t p0, int npc,
                                           int lg, bool head_mid, uint32_t a_rec, uint32_t a_col,
                                           uint32_t a_mask, uint32_t a_val, int lane,
@@ -809,22 +832,26 @@ __device__ __forceinline__ void lpp_chunk(const SpmvArgs &a, int64_t c, int64_t 
         // gathers are in flight before the first FMA; values still accumulate
         // in storage order
         if constexpr (R == 8) {  // pair slots: steps of 6 / 12 / 18 blocks
+            // (run plans keep the pair slots for 8-bit masks -- 128^3 f64 beta(8,8)
+            // 105.6 us with them, 117.9 us with run block slots -- and use run
+            // block slots where a step falls back to them)
+            constexpr bool PR = !RUN || sizeof(MT) == 1;
             if (maxlen <= 6) {
-                lpp_steps2<T, MT, R, 6, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+                lpp_steps2<T, MT, R, 6, PR, RUN>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else if (maxlen <= 9) {  // one step of block slots (beta(8,16) stencil rows)
-                lpp_steps2<T, MT, R, 9, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+                lpp_steps2<T, MT, R, 9, false, RUN>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else if (maxlen <= 12) {
-                lpp_steps2<T, MT, R, 12, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+                lpp_steps2<T, MT, R, 12, PR, RUN>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else {
-                lpp_steps2<T, MT, R, 18, true>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+                lpp_steps2<T, MT, R, 18, PR, RUN>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             }
         } else {
             if (maxlen <= 3) {
-                lpp_steps2<T, MT, R, 3, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+                lpp_steps2<T, MT, R, 3, false, RUN>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else if (maxlen <= 6) {
-                lpp_steps2<T, MT, R, 6, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+                lpp_steps2<T, MT, R, 6, false, RUN>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             } else {
-                lpp_steps2<T, MT, R, 9, false>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
+                lpp_steps2<T, MT, R, 9, false, RUN>(acc, maxlen, my, s, rr, lg, lane, vaddr, a_col, a_mask, x);
             }
         }
         for (int o = 1; o < G; o <<= 1) acc += __shfl_xor_sync(kFull, acc, o);
@@ -1576,7 +1603,9 @@ __device__ __forceinline__ void lbr_chunk(const SpmvArgs &a, int64_t c, int64_t 
 // lane-per-panel-row, balanced lane ranges and lane-per-block (no flat value
 // ranges); 1: flat value ranges only; 2: every mode (mixed plans and range
 // products); 3: lane-per-panel-row only; 4: lane-per-block-row rounds (LBR
-// plans; chunks holding empty panels fall back to lane-per-block).
+// plans; chunks holding empty panels fall back to lane-per-block); 6:
+// lane-per-panel-row only, every row mask one run of bits (immediate-offset
+// gathers, row_slots RUN).
 template <typename T, typename MT, int R, bool GENERIC, int MODE>
 // 168 registers: 12 warps per SM (3 CTAs x 4 warps) fit the register file;
 // the shared-memory ring allows no more
@@ -1688,6 +1717,9 @@ __global__ void __maxnreg__(sizeof(T) == 4 ? SPC5_K2_MAXREG_F32 : SPC5_K2_MAXREG
         } else if (MODE == 1) {
             fvr_chunk<T, MT, R, GENERIC, SPC5_FVR_U>(a, c, p0, n, head_mid, sh0, a_bits, a_rp,
                                                      a_col, a_mask, slot_values, lane, x, y);
+        } else if (MODE == 6) {  // lane-per-panel chunks of a run plan
+            lpp_chunk<T, MT, R, GENERIC, true>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3,
+                                               head_mid, a_rp, a_col, a_mask, a_val, lane, x, y);
         } else if (MODE < 4 && (MODE == 3 || (flags & 4))) {  // lane-per-panel chunk
             lpp_chunk<T, MT, R, GENERIC>(a, c, p0, (int)(pe - p0), (flags >> 3) & 3, head_mid,
                                          a_rp, a_col, a_mask, a_val, lane, x, y);
@@ -1871,6 +1903,8 @@ int launch_typed(const Matrix &m, const SpmvArgs &a, cudaStream_t st) {
     } else if (a.p_lo == 0 && a.p_hi == m.num_panels) {  // full product: the plan's modes only
         if (P.num_fvr == P.num_chunks)
             SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 1>, m, a, nc, st, ACC));
+        else if (P.num_lpp == P.num_chunks && P.runs)
+            SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 6>, m, a, nc, st));
         else if (P.num_lpp == P.num_chunks)
             SPC5_TRY(launch_ring_kernel(spmv_kernel<T, MT, R, false, 3>, m, a, nc, st));
         else if (P.num_fvr == 0)
