@@ -12,6 +12,9 @@
 #include <mutex>
 #include <new>
 #include <string>
+#include <thread>
+#include <vector>
+#include <cstring>
 
 #include "common.cuh"
 
@@ -20,7 +23,7 @@ struct HostPipe {
     int K = 0;                 // stages (0: not built)
     int64_t p[9], b[9], need[8];
     cudaStream_t h2d = nullptr, d2h = nullptr, comp = nullptr;
-    cudaEvent_t start = nullptr, done = nullptr, xin[8], yout[8];
+    cudaEvent_t start = nullptr, done = nullptr, xin[8], yout[8], ycopied[8];
 };
 
 // A handle: the matrix, its plan (built once, then read-only) and the
@@ -60,6 +63,7 @@ struct spc5_matrix {
             for (int k = 0; k < pipe.K; ++k) {
                 cudaEventDestroy(pipe.xin[k]);
                 cudaEventDestroy(pipe.yout[k]);
+                cudaEventDestroy(pipe.ycopied[k]);
             }
         }
     }
@@ -429,6 +433,57 @@ int spc5_spmv_panels(spc5_matrix_t h, int64_t panel_lo, int64_t panel_hi, const 
 // (spc5_spmv_panels), so y is bitwise the one-shot product's.  Measured on
 // config 2, beta(1,8): 0.55 ms per call against 0.73 ms for copy, product,
 // copy in sequence (x lands slower while the products saturate HBM).
+// Pageable host buffers (ordinary numpy arrays, what a drop-in caller of
+// kernels.py:119-129 passes).  cudaMemcpyAsync from pageable memory goes
+// through the driver's single-threaded staging at ~10 GB/s (45 GFLOP/s end to
+// end on the 400^3 matrix against 262 from pinned buffers), so large pageable
+// x / y are staged here instead: a team of host threads copies each pipeline
+// stage's piece of x into a process-wide pinned buffer while the previous
+// piece is on the wire, and copies each stage's y rows out of the pinned
+// buffer as its device-to-host copy completes.
+namespace {
+struct PinnedStage {
+    std::mutex mu;  // one pageable host product at a time per process
+    void *x = nullptr, *y = nullptr;
+    size_t xcap = 0, ycap = 0;
+    int grow(void **p, size_t *cap, size_t bytes) {
+        if (*cap >= bytes) return SPC5_OK;
+        if (*p) cudaFreeHost(*p);
+        *p = nullptr;
+        *cap = 0;
+        SPC5_CUDA(cudaHostAlloc(p, bytes, cudaHostAllocDefault));
+        *cap = bytes;
+        return SPC5_OK;
+    }
+};
+PinnedStage g_stage;
+
+bool is_pageable(const void *p) {
+    cudaPointerAttributes a{};
+    if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+        cudaGetLastError();
+        return true;
+    }
+    return a.type == cudaMemoryTypeUnregistered;
+}
+
+int host_threads() {
+    static const int n = [] {
+        if (const char *e = getenv("SPC5_HOST_THREADS")) return std::min(32, std::max(1, atoi(e)));
+        const unsigned hc = std::thread::hardware_concurrency();
+        return (int)std::min(8u, std::max(1u, hc / 2));
+    }();
+    return n;
+}
+
+// thread t of T copies its 64-byte-aligned share of [0, bytes)
+void copy_share(char *dst, const char *src, size_t bytes, int t, int T) {
+    const size_t lo = (bytes * (size_t)t / T) & ~(size_t)63, hi = t == T - 1 ? bytes
+                                                                            : (bytes * (size_t)(t + 1) / T) & ~(size_t)63;
+    if (hi > lo) std::memcpy(dst + lo, src + lo, hi - lo);
+}
+}  // namespace
+
 int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, void *stream) {
     g_launches = 0;
     if (!h) return fail(SPC5_EINVAL, "null handle");
@@ -457,6 +512,7 @@ int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, 
             for (int k = 0; k < K; ++k) {
                 SPC5_CUDA(cudaEventCreateWithFlags(&hp.xin[k], cudaEventDisableTiming));
                 SPC5_CUDA(cudaEventCreateWithFlags(&hp.yout[k], cudaEventDisableTiming));
+                SPC5_CUDA(cudaEventCreateWithFlags(&hp.ycopied[k], cudaEventDisableTiming));
             }
             hp.K = K;
         }
@@ -478,8 +534,59 @@ int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, 
     char *dx = static_cast<char *>(m.dx), *dy = static_cast<char *>(m.dy);
     const char *hx = static_cast<const char *>(h_x);
     char *hy = static_cast<char *>(h_y);
+    // large pageable buffers go through the pinned staging buffers, copied by a thread team
+    const bool big = xb + yb >= ((size_t)8 << 20) && !getenv("SPC5_NO_HOST_STAGING");
+    const bool px = big && is_pageable(h_x), py = big && is_pageable(h_y);
+    std::unique_lock<std::mutex> stage_lk(g_stage.mu, std::defer_lock);
+    const char *ux = hx;  // the caller's buffers
+    char *uy = hy;
+    const int T = host_threads();
+    std::vector<std::thread> team;
+    std::vector<std::atomic<int>> x_ready(px || (py && accumulate) ? hp.K : 0);
+    int64_t xlo[8], xhi[8];
+    if (px || py) {
+        stage_lk.lock();
+        if (px) SPC5_TRY(g_stage.grow(&g_stage.x, &g_stage.xcap, xb));
+        if (py) SPC5_TRY(g_stage.grow(&g_stage.y, &g_stage.ycap, yb));
+        if (px) hx = static_cast<const char *>(g_stage.x);
+        if (py) hy = static_cast<char *>(g_stage.y);
+        int64_t hv = 0;
+        for (int k = 0; k < hp.K; ++k) {
+            const int64_t want = k == hp.K - 1 ? m.num_cols : hp.need[k];
+            xlo[k] = hv;
+            xhi[k] = std::max(hv, want);
+            hv = xhi[k];
+        }
+        if (!x_ready.empty()) {
+            for (auto &c : x_ready) c.store(0);
+            char *sx = static_cast<char *>(g_stage.x), *sy = static_cast<char *>(g_stage.y);
+            for (int t = 0; t < T; ++t)
+                team.emplace_back([&, t, sx, sy] {
+                    for (int k = 0; k < hp.K; ++k) {
+                        if (px)
+                            copy_share(sx + xlo[k] * vb, ux + xlo[k] * vb,
+                                       (size_t)(xhi[k] - xlo[k]) * vb, t, T);
+                        if (py && accumulate) {
+                            int64_t r0, r1;
+                            rows(k, &r0, &r1);
+                            copy_share(sy + r0 * vb, uy + r0 * vb, (size_t)(r1 - r0) * vb, t, T);
+                        }
+                        x_ready[k].fetch_add(1, std::memory_order_release);
+                    }
+                });
+        }
+    }
+    struct Joiner {  // the team is joined on every exit path
+        std::vector<std::thread> &t;
+        ~Joiner() {
+            for (auto &th : t)
+                if (th.joinable()) th.join();
+        }
+    } joiner{team};
     int launches = 0;
     for (int k = 0; k < hp.K; ++k) {
+        if (!x_ready.empty())  // this stage's piece has been staged by every thread
+            while (x_ready[k].load(std::memory_order_acquire) < T) std::this_thread::yield();
         const int64_t want = k == hp.K - 1 ? m.num_cols : hp.need[k];
         if (want > have) {
             SPC5_CUDA(cudaMemcpyAsync(dx + have * vb, hx + have * vb, (size_t)(want - have) * vb,
@@ -507,11 +614,31 @@ int spc5_spmv_host(spc5_matrix_t h, const void *h_x, void *h_y, int accumulate, 
         if (r1 > r0)
             SPC5_CUDA(cudaMemcpyAsync(hy + r0 * vb, dy + r0 * vb, (size_t)(r1 - r0) * vb,
                                       cudaMemcpyDeviceToHost, hp.d2h));
+        if (py) SPC5_CUDA(cudaEventRecord(hp.ycopied[k], hp.d2h));
     }
     g_launches = launches;
     // the caller's stream completes with the last copy back
     SPC5_CUDA(cudaEventRecord(hp.done, hp.d2h));
     SPC5_CUDA(cudaStreamWaitEvent(st, hp.done, 0));
+    if (py) {
+        // each stage's rows leave the pinned buffer as soon as they have landed in it
+        for (auto &th : team)
+            if (th.joinable()) th.join();
+        team.clear();
+        std::atomic<int> bad{0};
+        for (int t = 0; t < T; ++t)
+            team.emplace_back([&, t] {
+                for (int k = 0; k < hp.K; ++k) {
+                    if (cudaEventSynchronize(hp.ycopied[k]) != cudaSuccess) bad.store(1);
+                    int64_t r0, r1;
+                    rows(k, &r0, &r1);
+                    copy_share(uy + r0 * vb, hy + r0 * vb, (size_t)(r1 - r0) * vb, t, T);
+                }
+            });
+        for (auto &th : team) th.join();
+        team.clear();
+        if (bad.load()) return fail(SPC5_ECUDA, "device-to-host copy of y failed");
+    }
     SPC5_CUDA(cudaStreamSynchronize(st));
     return SPC5_OK;
 }

@@ -252,3 +252,38 @@ def test_cli_bench_device_cuda(spc5, tmp_path, capsys):
                "--reps", "2", "--warmup", "1"])
     assert rc == 0
     assert main(["bench", "--device", "cpu", "--matrix", "dense:8"]) == 2
+
+
+def test_large_pageable_host_buffers_are_staged(spc5):
+    """x / y of >= 8 MB in ordinary (pageable) numpy arrays go through the
+    library's pinned staging buffers with a host thread team
+    (spc5_spmv_host): the result is bitwise the pinned-buffer call's, for
+    y = A.x and for the accumulating entry point."""
+    import torch
+    n = 1_300_000
+    rng = np.random.default_rng(21)
+    off = np.array([-3, 0, 1, 7, 1000])
+    ci = (np.arange(n)[:, None] + off[None, :])
+    ci = np.sort(np.clip(ci, 0, n - 1), axis=1)
+    keep = np.ones_like(ci, dtype=bool)
+    keep[:, 1:] = ci[:, 1:] != ci[:, :-1]
+    rp = np.zeros(n + 1, np.int64)
+    np.cumsum(keep.sum(axis=1), out=rp[1:])
+    m = Csr(n, n, rp, ci[keep].astype(np.int32), rng.uniform(-1, 1, int(keep.sum())))
+    x = rng.uniform(-1, 1, n)
+    for r in (1, 4):
+        s = spc5.csr_to_spc5(m, r, 8)
+        xp = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        xp.numpy()[:] = x
+        yp = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        spc5.spmv(s, xp.numpy(), yp.numpy())
+        y = spc5.spmv(s, x)  # pageable in, pageable out
+        assert y.tobytes() == yp.numpy().tobytes(), r
+        y_mixed = np.empty(n)
+        spc5.spmv(s, xp.numpy(), y_mixed)  # pinned in, pageable out
+        assert y_mixed.tobytes() == y.tobytes()
+        acc = np.full(n, 0.5)
+        spc5.spmv_spc5_scalar(s, x, acc)  # accumulate: y is read from and written to pageable memory
+        accp = torch.full((n,), 0.5, dtype=torch.float64).pin_memory()
+        spc5.spmv_spc5_scalar(s, xp.numpy(), accp.numpy())
+        assert acc.tobytes() == accp.numpy().tobytes()
