@@ -269,7 +269,7 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                                    const int64_t *__restrict__ chunk_p,
                                    const int64_t *__restrict__ rowptr,
                                    const int64_t *__restrict__ empty, int64_t ne, int lpr_split,
-                                   int lpr_bal_num, int lpr_bal_den, int fvr,
+                                   int lpr_bal_num, int lpr_bal_den, int fvr, int64_t min_lanes,
                                    const int64_t *__restrict__ chunk_v, uint8_t *flags) {
     const int64_t c = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
     if (c >= nc) return;
@@ -298,7 +298,7 @@ __global__ void chunk_flags_kernel(int64_t nc, int64_t nb, int64_t np, int r,
                 maxlen = max(maxlen, min(rowptr[p + 1], cb1) - max(rowptr[p], cb0));
             int lg = 0;  // G = 1 << lg lanes per panel row, each with >= 1 block
             while (lg < 3 && npc * r * (2 << lg) <= 32 && maxlen >= (2 << lg)) ++lg;
-            if (npc * r * (1 << lg) >= kLppMinLanes && maxlen <= 64 * (1 << lg) &&
+            if (npc * r * (1 << lg) >= min_lanes && maxlen <= 64 * (1 << lg) &&
                 maxlen * npc * lpr_bal_den <= lpr_bal_num * (cb1 - cb0) + 2 * lpr_bal_den * npc)
                 f |= 4 | (lg << 3) | (ends_clean ? 0 : 32);
         }
@@ -976,7 +976,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
             P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
             P.num_empty,
             (P.lbr || getenv("SPC5_NO_LPR")) ? -1 : (getenv("SPC5_LPR_SPLIT") ? 1 : 0), lpr_bal, 4,
-            P.lbr ? 0 : fvr_mode, P.chunk_v, P.chunk_flags);
+            P.lbr ? 0 : fvr_mode, kLppMinLanes, P.chunk_v, P.chunk_flags);
         SPC5_CUDA(cudaGetLastError());
         unsigned long long *d_st = nullptr, h_st[5] = {0, 0, 0, 0, 0};
         SPC5_TRY(dev_alloc(&d_st, 5));
@@ -1008,6 +1008,31 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
             SPC5_CUDA(cudaStreamSynchronize(st));
             dev_free(d_cl);
             P.num_fvr -= (int64_t)h_cl;
+        }
+        // A plan that is lane-per-panel-row but for a few chunks (panels of
+        // uneven length at grid faces: 796 of 2 M chunks on the 400^3 beta(8,8)
+        // stencil, 68 of 35 k on the 128^3 beta(2,16) one) takes those chunks as
+        // lane-per-panel-row too, balance rule and lane minimum waived: the
+        // whole plan then runs the LPP-only kernel, and the run-plan variant
+        // when its masks allow (400^3 beta(8,8) 3,335 -> 3,261 us).
+        if (!P.lbr && P.num_lpp < P.num_chunks && P.num_lpp * 50 >= P.num_chunks * 49 &&
+            !getenv("SPC5_NO_LPR") && !getenv("SPC5_NO_LPP_RELAX")) {
+            chunk_flags_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
+                P.num_chunks, nb, np, m.r, P.chunk_b, P.chunk_p, m.rowptr, P.empty_panels,
+                P.num_empty, getenv("SPC5_LPR_SPLIT") ? 1 : 0, 1 << 20, 4, 0, 1, P.chunk_v,
+                P.chunk_flags);
+            unsigned long long *d_st2 = nullptr, h_st2[3] = {0, 0, 0};
+            SPC5_TRY(dev_alloc(&d_st2, 3));
+            SPC5_CUDA(cudaMemsetAsync(d_st2, 0, 3 * sizeof(unsigned long long), st));
+            lpp_panels_kernel<<<(unsigned)cdiv(P.num_chunks, 256), 256, 0, st>>>(
+                P.num_chunks, P.chunk_p, P.chunk_flags, d_st2, d_st2 + 1, d_st2 + 2);
+            SPC5_CUDA(cudaGetLastError());
+            SPC5_CUDA(cudaMemcpyAsync(h_st2, d_st2, sizeof(h_st2), cudaMemcpyDeviceToHost, st));
+            SPC5_CUDA(cudaStreamSynchronize(st));
+            dev_free(d_st2);
+            P.max_lpp_panels = (int64_t)h_st2[0];
+            P.num_fvr = (int64_t)h_st2[1];
+            P.num_lpp = (int64_t)h_st2[2];
         }
         P.chunk_target = cb;
         auto a16 = [](int64_t v) { return (v + 15) / 16 * 16; };
