@@ -296,6 +296,8 @@ int launch_fill(const ConvArgs &a, int64_t nnz, int64_t nb, cudaStream_t st) {
     cap.entries = ((int)(erow * T * 1.25) + 128 + 3) / 4 * 4;
     cap.blocks = ((int)((double)nb / rows * T / R * 1.25) + 64 + 3) / 4 * 4;
     size_t smem = (size_t)cap.entries * (size_t)ebytes + (size_t)cap.blocks * (4 + R * mb) + 16;
+    // (Staging only the block outputs of R > 1 was slower too: 400^3 fill
+    // beta(2|4|8,8) 20.0 / 14.1 / 15.7 vs 15.6 / 12.1 / 13.5 ms direct.)
     // R > 1: the staged path measured slower than the direct walk (400^3 stencil
     // beta(8,8) fill 46 vs 18 ms, FEM beta(8,8) 7.5 vs 1.1 ms: the value
     // permutation through shared memory and CTAs of 64-128 threads cost more
