@@ -955,6 +955,30 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         P.split_len = INT64_MAX / 4;  // exact cuts bound every chunk: no forced splits
     }
     if (const char *e = getenv("SPC5_SLOT_B")) slot_cap = std::max(1024, atoi(e));
+    // run plans (knob SPC5_NO_RUN=1 keeps the general bit walk): is every row
+    // mask one contiguous run of bits?
+    bool masks_runs = false;
+    if (!getenv("SPC5_NO_RUN")) {
+        int *d_bad = nullptr, h_bad = 0;
+        SPC5_TRY(dev_alloc(&d_bad, 1));
+        SPC5_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
+        runs_kernel<<<(unsigned)std::min<int64_t>(cdiv(nb * m.r, 1024), 148 * 16), 256, 0, st>>>(
+            nb * m.r, m.vs, m.masks, d_bad);
+        SPC5_CUDA(cudaGetLastError());
+        SPC5_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
+        SPC5_CUDA(cudaStreamSynchronize(st));
+        dev_free(d_bad);
+        masks_runs = h_bad == 0;
+    }
+    // The run-plan kernel of fp32 beta(2,16) needs 119 registers: with slots of
+    // <= 7,040 B a fourth CTA fits each SM (16 warps instead of 12): 400^3
+    // 1,866 -> 1,707 us, 128^3 63.6 -> 59.0 us.  (beta(4,16) gains nothing,
+    // beta(8,16) and the f64 kernels keep 3 CTAs by their registers and only
+    // lose chunk size: 400^3 beta(1,8) 2,766 -> 4,914 us.)
+    int64_t lpp_cap = slot_cap;
+    if (masks_runs && m.value_bytes() == 4 && m.r == 2 && !getenv("SPC5_SLOT_B") &&
+        !getenv("SPC5_SLOT_KB"))
+        lpp_cap = std::min<int64_t>(lpp_cap, 7040);
     // irregular r = 1 matrices (block-count targets): slots <= 8 KB
     int64_t irr_cap = m.r == 1 ? std::min<int64_t>(slot_cap, 8192) : slot_cap;
     if (const char *e = getenv("SPC5_SLOT_B_IRR")) irr_cap = std::max(1024, atoi(e));
@@ -1052,7 +1076,8 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
         const bool regular = ppc <= 0 || P.max_chunk_blocks * 4 <= cb * 5;
         // FVR kernels of r = 8 keep their row sums in shared memory (r*256 B
         // per warp = r*128 B per ring slot): smaller slots keep 3 CTAs per SM
-        const int64_t cap = (ppc ? slot_cap : irr_cap) - (P.num_fvr && m.r == 8 ? m.r * 128 : 0);
+        const int64_t cap = (ppc > 0 ? lpp_cap : ppc < 0 ? slot_cap : irr_cap) -
+                            (P.num_fvr && m.r == 8 ? m.r * 128 : 0);
         if (!regular) {  // fewer panels per chunk only averages worse: go to block targets
             while (ti + 1 < targets.size() && targets[ti + 1].ppc > 0) ++ti;
         }
@@ -1064,20 +1089,7 @@ int build_plan(Matrix &m, bool validate, cudaStream_t st) {
     }
     if (P.slot_bytes > 14 * 1024)
         return fail(SPC5_EINVAL, "a chunk of this matrix does not fit the shared-memory ring");
-    // run plans (knob SPC5_NO_RUN=1 keeps the general bit walk)
-    P.runs = false;
-    if (P.num_lpp == P.num_chunks && !getenv("SPC5_NO_RUN")) {
-        int *d_bad = nullptr, h_bad = 0;
-        SPC5_TRY(dev_alloc(&d_bad, 1));
-        SPC5_CUDA(cudaMemsetAsync(d_bad, 0, sizeof(int), st));
-        runs_kernel<<<(unsigned)std::min<int64_t>(cdiv(nb * m.r, 1024), 148 * 16), 256, 0, st>>>(
-            nb * m.r, m.vs, m.masks, d_bad);
-        SPC5_CUDA(cudaGetLastError());
-        SPC5_CUDA(cudaMemcpyAsync(&h_bad, d_bad, sizeof(int), cudaMemcpyDeviceToHost, st));
-        SPC5_CUDA(cudaStreamSynchronize(st));
-        dev_free(d_bad);
-        P.runs = h_bad == 0;
-    }
+    P.runs = masks_runs && P.num_lpp == P.num_chunks;
     // panel-start bitmap
     const int off32 = (int)(((m.block_base % 32) + 32) % 32);
     const int64_t ng = cdiv(nb + off32, 32);
