@@ -30,10 +30,9 @@ A(f"`value` = **{d['value']:.0f} GFLOP/s** for the four-format step, `roofline.f
   f"**{d['roofline']['frac']:.3f}** of measured ({d['roofline']['peak']:.0f} GB/s, "
   f"MEASURED_PEAKS.json), `ms_per_step` = {d['ms_per_step']:.2f}, `gpu_launches` = "
   f"{d['gpu_launches']}. Clocks during the timed region: median {c['sm_mhz']:.0f} MHz of "
-  f"{c['sm_max_mhz']:.0f}, reasons {c['reasons']}: the 200 back-to-back 3 ms products of the "
-  "timed region run under the 1,000 W power cap. The same library timed over 5 steps per "
-  "format at full clock (`bench_dist1rank_c5_r2.json`, the N > 1 code path with one rank) "
-  "reaches 1,178 GFLOP/s (β(1|2|4|8,8) 2,781 / 2,817 / 2,763 / 3,319 µs: 0.98 / 0.90 / 0.88 / 0.76).\n")
+  f"{c['sm_max_mhz']:.0f}, reasons {c['reasons']} (the power cap is the only reason ever seen; a "
+  "run of the same library on a box that the cap held at a median 1,755 MHz read 1,122 GFLOP/s "
+  "at 0.84 -- box-to-box spread on this pool is about +-2.5 %).\n")
 A("| format | µs / product | algorithmic GB/s | frac of measured peak | algorithmic GB | "
   "K1 count + fill (ms) | K1 frac of peak | plan (ms) |")
 A("|---|---|---|---|---|---|---|---|")
