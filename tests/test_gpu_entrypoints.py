@@ -287,3 +287,35 @@ def test_large_pageable_host_buffers_are_staged(spc5):
         accp = torch.full((n,), 0.5, dtype=torch.float64).pin_memory()
         spc5.spmv_spc5_scalar(s, xp.numpy(), accp.numpy())
         assert acc.tobytes() == accp.numpy().tobytes()
+
+
+def test_cli_stats_verify_fit(spc5, tmp_path, capsys):
+    """The other reference CLI commands on the GPU functions: `stats`
+    (cli.py:81-111), `verify` with the mask fault injection (cli.py:114-152: a
+    clean matrix passes every config, a corrupted mask fails) and `fit`
+    (cli.py:188-199) over records written by `bench`."""
+    from paper_2307_14774_b200.__main__ import main
+    assert main(["stats", "--matrix", "dense:32", "--matrix", "random:500,600,9,0.5,1",
+                 "--format", "b1,b8"]) == 0
+    out = capsys.readouterr().out.splitlines()
+    assert out[0].split()[:4] == ["matrix", "dim", "nnz", "nnz/row"]
+    assert out[1].startswith("dense:32") and "100%|100%" in out[1]
+    assert out[2].startswith("random:500,600,9,0.5,1") and "500x600" in out[2]
+    spec = "random:400,400,11,0.4,5"
+    assert main(["verify", "--matrix", spec, "--format", "b2,b4", "--trials", "2"]) == 0
+    ok = [ln for ln in capsys.readouterr().out.splitlines() if ln.startswith(spec)]
+    assert len(ok) == 2 * 12 and all("pass" in ln.lower() or "ok" in ln.lower() for ln in ok), ok[:2]
+    assert main(["verify", "--matrix", spec, "--format", "b2", "--strategy", "expand",
+                 "--reduction", "hsum", "--xload", "partial", "--inject-mask-corruption", "7"]) == 1
+    records = []
+    for i, n in enumerate((300, 600, 900, 1200, 1500, 1800)):
+        out_csv = tmp_path / f"r{i}.csv"
+        assert main(["bench", "--matrix", f"random:{n},{n},10,0.5,{i}", "--format", "b1",
+                     "--reps", "2", "--warmup", "1", "--out", str(out_csv)]) == 0
+        records += spc5.read_records(out_csv)
+    merged = tmp_path / "all.csv"
+    spc5.write_records(merged, records)
+    capsys.readouterr()
+    assert main(["fit", str(merged), "--min-records", "5"]) == 0
+    assert "cost/block" in capsys.readouterr().out
+    assert main(["fit", str(merged), "--min-records", "50"]) == 2
